@@ -1,0 +1,165 @@
+/* pbh-b200 — C-ABI of the B200-native parBucketHeap hot path.
+ *
+ * Drop-in boundary for the reference's priority-queue + SSSP API
+ * (/root/reference/proj/include/pbh/*.hpp). Plain pointers and sizes only;
+ * no torch or CUDA types. Every entry point returns a pbh_status; the message
+ * of the last failure on the calling thread is pbh_last_error().
+ *
+ * Status codes map one-to-one onto the reference's exception types
+ * (/root/reference/proj/include/pbh/error.hpp:9-30):
+ *   PBH_EMPTY        -> pbh::EmptyHeapError      (error.hpp:9-12)
+ *   PBH_PRECONDITION -> pbh::PreconditionError   (error.hpp:14-18)
+ *   PBH_INVARIANT    -> pbh::InvariantError      (error.hpp:20-24)
+ *   PBH_TRACE        -> pbh::TraceError{op_index}(error.hpp:26-30)
+ * plus PBH_CUDA / PBH_OOM for device failures (no reference equivalent).
+ *
+ * Threading: a handle owns one CUDA stream and is not thread-safe; distinct
+ * handles may be used concurrently ("externally a single-client, blocking
+ * interface"). Host pointers are copied; *_device variants take
+ * device pointers already resident in HBM on the handle's device.
+ */
+#ifndef PBH_GPU_H
+#define PBH_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PBH_OK = 0,
+  PBH_EMPTY = 1,
+  PBH_PRECONDITION = 2,
+  PBH_INVARIANT = 3,
+  PBH_TRACE = 4,
+  PBH_CUDA = 5,
+  PBH_OOM = 6
+} pbh_status;
+
+typedef struct pbh_heap pbh_heap;
+
+/* Message of the last non-OK status returned on this thread. */
+const char* pbh_last_error(void);
+
+/* Library version string. */
+const char* pbh_version(void);
+
+/* ---- heap lifecycle ---------------------------------------------------
+ * Replaces pbh::Engine::Engine(EngineConfig{d, workers, debug_assertions})
+ * (engine.hpp:49, engine.cpp:22-30) and BucketHeap(HeapConfig)
+ * (bucket_heap.cpp:11-15): d must be in [1, 2^40] else PBH_PRECONDITION.
+ * key_universe: initial size of the per-key position index (keys are
+ * u32 values); 0 picks a default. The index grows on demand for update
+ * keys beyond it; deletes of keys beyond it are no-ops (absent values).
+ * debug_checks mirrors EngineConfig::debug_assertions with workers == 1
+ * (trace_checks, engine.cpp:23-24): priority increases are rejected. */
+pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int debug_checks,
+                           pbh_heap** out);
+pbh_status pbh_heap_destroy(pbh_heap* h);
+
+/* ---- single-client ops (engine.hpp:56-61) ------------------------------ */
+/* Engine::update(Element) (engine.cpp:90-93; bucket_heap.cpp:101-111):
+ * insert-if-absent / decrease-key. Re-inserting an extracted or deleted
+ * value -> PBH_PRECONDITION (bucket_heap.cpp:55-58). */
+pbh_status pbh_heap_update(pbh_heap* h, uint32_t value, uint64_t priority);
+/* Engine::bulk_update(span) (engine.cpp:95-98; bucket_heap.cpp:127-146):
+ * 1 <= n <= d, values strictly increasing, else PBH_PRECONDITION. */
+pbh_status pbh_heap_bulk_update(pbh_heap* h, const uint32_t* values, const uint64_t* priorities,
+                                uint64_t n);
+/* Engine::extract_min() (engine.cpp:100-104): PBH_EMPTY when no live value. */
+pbh_status pbh_heap_extract_min(pbh_heap* h, uint32_t* value, uint64_t* priority);
+/* BucketHeap::find_min() (bucket_heap.cpp:66-77). */
+pbh_status pbh_heap_find_min(pbh_heap* h, uint32_t* value, uint64_t* priority);
+/* Engine::delete_value(Value) (engine.cpp:106-109): absent -> no-op. */
+pbh_status pbh_heap_delete(pbh_heap* h, uint32_t value);
+/* Engine::live_size() (engine.hpp:61). */
+pbh_status pbh_heap_live_size(pbh_heap* h, int64_t* n);
+/* Engine::drain() (engine.cpp:138-150): flush all signal buffers. */
+pbh_status pbh_heap_drain(pbh_heap* h);
+
+/* Engine::snapshot_metrics() (engine.cpp:152-163), schema pbh.metrics.v1:
+ * ops, resolves/touches per level for levels [0, *n_levels). Arrays must
+ * hold PBH_GPU_MAX_LEVELS entries. */
+#define PBH_GPU_MAX_LEVELS 24
+pbh_status pbh_heap_metrics(pbh_heap* h, uint64_t* ops, uint64_t* resolves_per_level,
+                            uint64_t* touches_per_level, uint32_t* n_levels);
+
+/* Structural audit (BucketHeap::check_invariants, bucket_heap.cpp:302-409)
+ * restated for the (priority, value)-sorted SoA levels: sortedness, splitter
+ * separation, capacity, live count. Returns the number of violations in
+ * *n_violations (0 = clean). Blocking; copies the levels to the host. */
+pbh_status pbh_heap_check_invariants(pbh_heap* h, uint64_t* n_violations);
+
+/* ---- op traces (trace_format.hpp:16-33; engine.cpp:207-226) -------------
+ * Flat trace: op i has kind kinds[i] in {'U','B','E','D'} and owns elements
+ * [offsets[i], offsets[i+1]) of values/priorities (D: one value, E: none).
+ * Engine::run_trace: replays the whole trace in ONE device submission, then
+ * drains. out_values/out_priorities receive the extracted elements in order
+ * (capacity = number of 'E' ops); *n_out their count. On an op failure the
+ * status is PBH_TRACE and *failed_op the op index (TraceError::op_index);
+ * out arrays then hold the extractions before it. wall_ms (nullable) is the
+ * device-timed replay, like Metrics::wall_ms. */
+pbh_status pbh_heap_run_trace(pbh_heap* h, uint64_t n_ops, const uint8_t* kinds,
+                              const uint64_t* offsets, const uint32_t* values,
+                              const uint64_t* priorities, uint32_t* out_values,
+                              uint64_t* out_priorities, uint64_t* n_out, uint64_t* failed_op,
+                              double* wall_ms);
+/* Same with every pointer in device memory (inputs resident in HBM). */
+pbh_status pbh_heap_run_trace_device(pbh_heap* h, uint64_t n_ops, const uint8_t* d_kinds,
+                                     const uint64_t* d_offsets, const uint32_t* d_values,
+                                     const uint64_t* d_priorities, uint32_t* d_out_values,
+                                     uint64_t* d_out_priorities, uint64_t* n_out,
+                                     uint64_t* failed_op, double* wall_ms);
+
+/* ---- SSSP (sssp.hpp:13-29) ----------------------------------------------
+ * par_dijkstra(g, source, EngineConfig{d}, dag_mode) (sssp.cpp:21-69) as
+ * ONE persistent CTA per source. CSR: offsets u64[V+1], targets u32[E],
+ * weights u32[E] (graphs.hpp:11-20). d == 0 selects max(1, max out-degree).
+ * Outputs (caller-allocated, nullable except dist): dist u64[V] (kInfDist =
+ * ~0 where unreachable), parent u32[V] (predecessor on a shortest-path tree;
+ * source -> source, unreachable -> 0xFFFFFFFF; an extension: SsspResult has
+ * no parent field), settled u32[V] (extraction order), *n_settled, *rounds,
+ * *ops (Metrics::ops). debug_checks as in pbh_heap_create. */
+typedef struct {
+  uint32_t vertex_count;
+  uint64_t edge_count;
+  const uint64_t* offsets;
+  const uint32_t* targets;
+  const uint32_t* weights;
+} pbh_csr;
+
+pbh_status pbh_sssp(const pbh_csr* g, uint32_t source, uint64_t d, int dag_mode, int device,
+                    uint64_t* dist, uint32_t* parent, uint32_t* settled, uint64_t* n_settled,
+                    uint64_t* rounds, uint64_t* ops);
+
+/* Multi-source batch (BASELINE config 5): n_sources independent
+ * par_dijkstra runs. Sources are dealt contiguously over `n_devices`
+ * devices; each device holds a replica of the CSR and runs its sources as
+ * concurrent persistent CTAs; results are gathered to the host. dist is
+ * n_sources x V (row-major), parent likewise (nullable). */
+pbh_status pbh_sssp_multi(const pbh_csr* g, const uint32_t* sources, uint64_t n_sources,
+                          uint64_t d, const int* devices, int n_devices, uint64_t* dist,
+                          uint32_t* parent);
+
+/* Device-resident SSSP context for timing with inputs already in HBM:
+ * the CSR is uploaded once; each pbh_sssp_ctx_run solves n_sources sources
+ * on this device and leaves dist/parent in device memory. */
+typedef struct pbh_sssp_ctx pbh_sssp_ctx;
+pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_t max_sources,
+                               pbh_sssp_ctx** out);
+pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n_sources,
+                            int dag_mode, double* device_ms);
+pbh_status pbh_sssp_ctx_fetch(pbh_sssp_ctx* c, uint64_t source_slot, uint64_t* dist,
+                              uint32_t* parent, uint32_t* settled, uint64_t* n_settled,
+                              uint64_t* rounds, uint64_t* ops);
+pbh_status pbh_sssp_ctx_destroy(pbh_sssp_ctx* c);
+
+/* distance_checksum (sssp.cpp:174-183): FNV-1a over the distance bytes. */
+uint64_t pbh_distance_checksum(const uint64_t* dist, uint64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

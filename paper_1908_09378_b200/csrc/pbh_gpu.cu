@@ -1,0 +1,1044 @@
+// pbh-b200 host runtime: implements include/pbh_gpu.h over the kernels of
+// pbh_kernels.cuh. Owns device memory (levels, position index, staging),
+// launch configuration, the NEED_GROW resume loop and error mapping.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/pbh_gpu.h"
+#include "pbh_kernels.cuh"
+
+using namespace pbh_dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+pbh_status set_err(pbh_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return set_err(e_ == cudaErrorMemoryAllocation ? PBH_OOM : PBH_CUDA,              \
+                     std::string(#call) + ": " + cudaGetErrorString(e_));               \
+  } while (0)
+
+constexpr int VT = 4;
+constexpr u32 kSmemLimit = 227 * 1024;
+
+u64 pow2_at_least(u64 x) {
+  u64 p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+u32 a16(u64 x) { return (u32)((x + 15) & ~u64(15)); }
+
+template <int NT>
+size_t heap_smem_bytes() {
+  return sizeof(HeapSmem<NT, VT>);
+}
+
+size_t heap_smem_bytes_nt(int nt) {
+  switch (nt) {
+    case 32: return heap_smem_bytes<32>();
+    case 256: return heap_smem_bytes<256>();
+    default: return heap_smem_bytes<1024>();
+  }
+}
+
+SmLayout make_layout(int nt, u32 cap0, u32 bc, u32 d, bool sssp) {
+  SmLayout L{};
+  u32 off = a16(heap_smem_bytes_nt(nt));
+  const u32 base = off;
+  L.off_b0k0 = off; off += a16((u64)cap0 * 4);
+  L.off_b0k1 = off; off += a16((u64)cap0 * 4);
+  L.off_b0p0 = off; off += a16((u64)cap0 * 8);
+  L.off_b0p1 = off; off += a16((u64)cap0 * 8);
+  L.off_bk = off; off += a16((u64)bc * 4);
+  L.off_bp = off; off += a16((u64)bc * 8);
+  L.off_pk = off; off += a16((u64)bc * 4);
+  L.off_pp = off; off += a16((u64)bc * 8);
+  L.off_rm = off; off += a16(cap0);
+  if (sssp) {
+    const u64 cc = (u64)d + nt;
+    L.off_ck = off; off += a16(cc * 4);
+    L.off_cp = off; off += a16(cc * 8);
+    L.off_co = off; off += a16(cc * 8);
+    L.off_cs = off; off += a16(cc * 4);
+  }
+  if (off <= kSmemLimit) {
+    L.use_smem = 1;
+    L.total = off;
+  } else {
+    L.use_smem = 0;
+    L.total = base;
+  }
+  return L;
+}
+
+int pick_nt(u64 d) {
+  if (const char* e = getenv("PBH_NT")) return atoi(e);
+  if (d <= 32) return 32;
+  if (d <= 256) return 256;
+  return 1024;
+}
+
+u32 pick_cap0(u64 d) {
+  u64 c0min = 256;
+  if (const char* e = getenv("PBH_CAP0_MIN")) c0min = strtoull(e, nullptr, 10);
+  u64 c = std::max<u64>(2 * d, c0min);
+  c = std::min<u64>(c, 1ull << 22);
+  return (u32)c;
+}
+
+// ------------------------------------------------------------ kernel table
+template <int NT>
+cudaError_t launch_trace(const SmLayout& L, cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr,
+                         u64 b, u64 e, u32* ov, u64* op, pbh_kstatus* ks, u32 internal) {
+  auto fn = k_trace<NT, VT>;
+  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+  if (err != cudaSuccess) return err;
+  fn<<<1, NT, L.total, st>>>(g, tr, b, e, ov, op, ks, L, internal);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trace_nt(int nt, const SmLayout& L, cudaStream_t st, pbh_heap_dev* g,
+                            pbh_trace_dev tr, u64 b, u64 e, u32* ov, u64* op, pbh_kstatus* ks,
+                            u32 internal) {
+  switch (nt) {
+    case 32: return launch_trace<32>(L, st, g, tr, b, e, ov, op, ks, internal);
+    case 256: return launch_trace<256>(L, st, g, tr, b, e, ov, op, ks, internal);
+    default: return launch_trace<1024>(L, st, g, tr, b, e, ov, op, ks, internal);
+  }
+}
+
+template <int NT>
+cudaError_t launch_sssp(const SmLayout& L, cudaStream_t st, u32 grid, pbh_heap_dev* heaps,
+                        const u64* off, const u32* tgt, const u32* w, u32 V, const u32* src,
+                        u64* dist, u32* settled, SsspState* sst, u32 dag, u32 maxdeg) {
+  auto fn = k_sssp<NT, VT>;
+  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+  if (err != cudaSuccess) return err;
+  fn<<<grid, NT, L.total, st>>>(heaps, off, tgt, w, V, src, dist, settled, sst, dag, maxdeg, L);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sssp_nt(int nt, const SmLayout& L, cudaStream_t st, u32 grid,
+                           pbh_heap_dev* heaps, const u64* off, const u32* tgt, const u32* w, u32 V,
+                           const u32* src, u64* dist, u32* settled, SsspState* sst, u32 dag,
+                           u32 maxdeg) {
+  switch (nt) {
+    case 32: return launch_sssp<32>(L, st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, dag, maxdeg);
+    case 256: return launch_sssp<256>(L, st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, dag, maxdeg);
+    default: return launch_sssp<1024>(L, st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, dag, maxdeg);
+  }
+}
+
+__global__ void k_finalize_parent(const pbh_idx_entry* idx, u32 V, u32* parent) {
+  for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < V; v += (u64)gridDim.x * blockDim.x) {
+    const pbh_idx_entry e = idx[v];
+    parent[v] = e.state == PBH_ST_DEAD ? e.parent : 0xffffffffu;
+  }
+}
+
+__global__ void k_max_degree(const u64* off, u32 V, unsigned long long* out) {
+  u64 best = 0;
+  for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < V; v += (u64)gridDim.x * blockDim.x)
+    best = max(best, off[v + 1] - off[v]);
+  atomicMax(out, (unsigned long long)best);
+}
+
+const char* detail_message(u32 detail) {
+  switch (detail) {
+    case PBH_ERR_EMPTY_HEAP: return "extract_min: heap is empty";
+    case PBH_ERR_EMPTY_BATCH: return "bulk_update: empty batch";
+    case PBH_ERR_BATCH_TOO_BIG: return "bulk_update: batch larger than d";
+    case PBH_ERR_UNSORTED: return "bulk_update: batch must be value-sorted with unique values";
+    case PBH_ERR_REINSERT: return "update: value was already extracted or deleted; re-insertion is unsupported";
+    case PBH_ERR_INCREASE: return "update: priority increase";
+    case PBH_ERR_INVARIANT: return "internal invariant violated";
+    case PBH_ERR_OVERFLOW: return "sssp: distance accumulation overflow";
+    case PBH_ERR_KEY_RANGE: return "update: value outside the position index";
+    case PBH_ERR_BAD_OP: return "unknown op kind";
+    default: return "error";
+  }
+}
+
+// ----------------------------------------------------------- device heap
+// One heap's device allocations. Used by pbh_heap (one) and SSSP contexts
+// (one per source slot).
+struct DevHeap {
+  pbh_heap_dev hd{};     // host mirror of the header (pointers + caps)
+  pbh_heap_dev* dev = nullptr;  // header in HBM (standalone) or slot in an array
+  std::vector<void*> allocs;
+  u32 bc = 0;  // batch capacity (pow2)
+
+  pbh_status alloc(void** p, size_t bytes) {
+    CK(cudaMalloc(p, bytes ? bytes : 16));
+    allocs.push_back(*p);
+    return PBH_OK;
+  }
+  void free_all() {
+    for (void* p : allocs) cudaFree(p);
+    allocs.clear();
+  }
+};
+
+pbh_status alloc_level(DevHeap& H, u32 i) {
+  pbh_level_bufs& b = H.hd.lv[i];
+  const u64 cap = i == 0 ? H.hd.cap0 : (u64)H.hd.cap0 << (2 * i);
+  if (cap >= (1ull << 31)) return set_err(PBH_OOM, "level capacity exceeds the 2^31 element limit");
+  b.cap_b = (u32)cap;
+  b.buf_s = i == 0 ? 0 : (u32)cap;
+  for (int s = 0; s < 2; ++s) {
+    pbh_status st;
+    if ((st = H.alloc((void**)&b.bk[s], cap * 4))) return st;
+    if ((st = H.alloc((void**)&b.bp[s], cap * 8))) return st;
+    if (i > 0) {
+      if ((st = H.alloc((void**)&b.sk[s], (u64)b.buf_s * 4))) return st;
+      if ((st = H.alloc((void**)&b.sp[s], (u64)b.buf_s * 8))) return st;
+    } else {
+      b.sk[s] = nullptr;
+      b.sp[s] = nullptr;
+    }
+  }
+  pbh_level_state& t = H.hd.st[i];
+  t = pbh_level_state{};
+  t.spl_inf = 1;
+  H.hd.n_levels = std::max<u32>(H.hd.n_levels, i + 1);
+  return PBH_OK;
+}
+
+pbh_status alloc_scratch(DevHeap& H, u32 bc, u32 nt) {
+  pbh_status st;
+  H.bc = bc;
+  if ((st = H.alloc((void**)&H.hd.g_bk, (u64)bc * 4))) return st;
+  if ((st = H.alloc((void**)&H.hd.g_bp, (u64)bc * 8))) return st;
+  if ((st = H.alloc((void**)&H.hd.g_pk, (u64)bc * 4))) return st;
+  if ((st = H.alloc((void**)&H.hd.g_pp, (u64)bc * 8))) return st;
+  if ((st = H.alloc((void**)&H.hd.g_rm, H.hd.cap0))) return st;
+  CK(cudaMemset(H.hd.g_rm, 0, H.hd.cap0));
+  const u64 cc = (u64)H.hd.d + nt;
+  if ((st = H.alloc((void**)&H.hd.g_ck, cc * 4))) return st;
+  if ((st = H.alloc((void**)&H.hd.g_cp, cc * 8))) return st;
+  if ((st = H.alloc((void**)&H.hd.g_co, cc * 8))) return st;
+  if ((st = H.alloc((void**)&H.hd.g_cs, cc * 4))) return st;
+  return PBH_OK;
+}
+
+// Initialise a heap: header, n_levels levels, scratch, index of `universe`.
+pbh_status init_heap(DevHeap& H, u64 d, u32 cap0, u32 bc, u32 nt, u64 universe, int debug,
+                     u32 n_levels, pbh_heap_dev* dev_slot) {
+  std::memset(&H.hd, 0, sizeof(H.hd));
+  H.hd.d = (u32)std::min<u64>(d, 0xffffffffu);
+  H.hd.cap0 = cap0;
+  H.hd.debug_checks = debug ? 1 : 0;
+  for (u32 i = 0; i < PBH_MAX_LEVELS; ++i) H.hd.st[i].spl_inf = 1;
+  pbh_status st;
+  for (u32 i = 0; i < n_levels; ++i)
+    if ((st = alloc_level(H, i))) return st;
+  if ((st = alloc_scratch(H, bc, nt))) return st;
+  H.hd.universe = universe;
+  if ((st = H.alloc((void**)&H.hd.idx, universe * sizeof(pbh_idx_entry)))) return st;
+  CK(cudaMemset(H.hd.idx, 0xff, universe * sizeof(pbh_idx_entry)));
+  if (dev_slot) {
+    H.dev = dev_slot;
+  } else {
+    if ((st = H.alloc((void**)&H.dev, sizeof(pbh_heap_dev)))) return st;
+  }
+  CK(cudaMemcpy(H.dev, &H.hd, sizeof(pbh_heap_dev), cudaMemcpyHostToDevice));
+  return PBH_OK;
+}
+
+// Pull the mutable header back, add one level, push it again.
+pbh_status grow_levels(DevHeap& H, cudaStream_t s) {
+  CK(cudaMemcpyAsync(&H.hd, H.dev, sizeof(pbh_heap_dev), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (H.hd.n_levels >= PBH_MAX_LEVELS) return set_err(PBH_OOM, "level limit reached");
+  pbh_status st = alloc_level(H, H.hd.n_levels);
+  if (st) return st;
+  CK(cudaMemcpyAsync(H.dev, &H.hd, sizeof(pbh_heap_dev), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  return PBH_OK;
+}
+
+pbh_status grow_universe(DevHeap& H, cudaStream_t s, u64 want) {
+  CK(cudaMemcpyAsync(&H.hd, H.dev, sizeof(pbh_heap_dev), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (want <= H.hd.universe) return PBH_OK;
+  u64 nu = std::max<u64>(pow2_at_least(want), 2 * H.hd.universe);
+  nu = std::min<u64>(nu, 1ull << 32);
+  pbh_idx_entry* ni = nullptr;
+  CK(cudaMalloc(&ni, nu * sizeof(pbh_idx_entry)));
+  CK(cudaMemsetAsync(ni, 0xff, nu * sizeof(pbh_idx_entry), s));
+  CK(cudaMemcpyAsync(ni, H.hd.idx, H.hd.universe * sizeof(pbh_idx_entry),
+                     cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  auto it = std::find(H.allocs.begin(), H.allocs.end(), (void*)H.hd.idx);
+  if (it != H.allocs.end()) {
+    cudaFree(*it);
+    *it = ni;
+  }
+  H.hd.idx = ni;
+  H.hd.universe = nu;
+  CK(cudaMemcpyAsync(H.dev, &H.hd, sizeof(pbh_heap_dev), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  return PBH_OK;
+}
+
+}  // namespace
+
+// =========================================================================
+// heap handle
+// =========================================================================
+struct pbh_heap {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  u64 d = 1;
+  int nt = 32;
+  DevHeap H;
+  SmLayout layout{};
+  pbh_kstatus* d_ks = nullptr;
+  pbh_kstatus* h_ks = nullptr;  // pinned
+  // staging for host traces
+  u64 st_ops = 0, st_el = 0, st_out = 0;
+  u8* d_kinds = nullptr;
+  u64* d_off = nullptr;
+  u32* d_vals = nullptr;
+  u64* d_prios = nullptr;
+  u32* d_ov = nullptr;
+  u64* d_op = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+pbh_status ensure_staging(pbh_heap* h, u64 n_ops, u64 n_el, u64 n_out) {
+  if (n_ops > h->st_ops) {
+    cudaFree(h->d_kinds);
+    cudaFree(h->d_off);
+    h->st_ops = std::max<u64>(pow2_at_least(n_ops), 64);
+    CK(cudaMalloc(&h->d_kinds, h->st_ops));
+    CK(cudaMalloc(&h->d_off, (h->st_ops + 1) * 8));
+  }
+  if (n_el > h->st_el) {
+    cudaFree(h->d_vals);
+    cudaFree(h->d_prios);
+    h->st_el = std::max<u64>(pow2_at_least(n_el), 64);
+    CK(cudaMalloc(&h->d_vals, h->st_el * 4));
+    CK(cudaMalloc(&h->d_prios, h->st_el * 8));
+  }
+  if (n_out > h->st_out) {
+    cudaFree(h->d_ov);
+    cudaFree(h->d_op);
+    h->st_out = std::max<u64>(pow2_at_least(n_out), 64);
+    CK(cudaMalloc(&h->d_ov, h->st_out * 4));
+    CK(cudaMalloc(&h->d_op, h->st_out * 8));
+  }
+  return PBH_OK;
+}
+
+// Make sure the batch scratch can hold batches of up to n elements.
+pbh_status ensure_batch(pbh_heap* h, u64 n) {
+  if (n <= h->H.bc) return PBH_OK;
+  u32 bc = (u32)pow2_at_least(n);
+  DevHeap& H = h->H;
+  CK(cudaMemcpyAsync(&H.hd, H.dev, sizeof(pbh_heap_dev), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  pbh_status st;
+  if ((st = H.alloc((void**)&H.hd.g_bk, (u64)bc * 4))) return st;
+  if ((st = H.alloc((void**)&H.hd.g_bp, (u64)bc * 8))) return st;
+  if ((st = H.alloc((void**)&H.hd.g_pk, (u64)bc * 4))) return st;
+  if ((st = H.alloc((void**)&H.hd.g_pp, (u64)bc * 8))) return st;
+  H.bc = bc;
+  CK(cudaMemcpyAsync(H.dev, &H.hd, sizeof(pbh_heap_dev), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  h->layout = make_layout(h->nt, H.hd.cap0, H.bc, H.hd.d, false);
+  return PBH_OK;
+}
+
+// Run ops [0, n_ops) of a device trace with the NEED_GROW / KEY_RANGE resume
+// loop. host_vals: host copy of the values (for universe growth) or null.
+pbh_status exec_trace(pbh_heap* h, u64 n_ops, pbh_trace_dev tr, u32* d_ov, u64* d_op,
+                      u64* n_out, u64* failed_op, u32 internal, double* wall_ms,
+                      const u8* host_kinds, const u64* host_off, const u32* host_vals) {
+  CK(cudaMemsetAsync(h->d_ks, 0, sizeof(pbh_kstatus), h->stream));
+  u64 begin = 0;
+  double ms_total = 0;
+  for (int guard = 0; guard < 4096; ++guard) {
+    if (begin >= n_ops) break;
+    CK(cudaEventRecord(h->ev0, h->stream));
+    CK(launch_trace_nt(h->nt, h->layout, h->stream, h->H.dev, tr, begin, n_ops, d_ov, d_op,
+                       h->d_ks, internal));
+    CK(cudaEventRecord(h->ev1, h->stream));
+    CK(cudaMemcpyAsync(h->h_ks, h->d_ks, sizeof(pbh_kstatus), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    ms_total += ms;
+    const pbh_kstatus ks = *h->h_ks;
+    if (ks.status == 0) break;
+    if (ks.status == 7) {  // NEED_GROW
+      pbh_status st = grow_levels(h->H, h->stream);
+      if (st) return st;
+      begin = ks.failed_op;
+      CK(cudaMemsetAsync(&h->d_ks->status, 0, 4, h->stream));
+      continue;
+    }
+    if (ks.detail == PBH_ERR_KEY_RANGE) {
+      // grow the index to cover every key of the failing op
+      const u64 op = ks.failed_op;
+      u64 b, e;
+      std::vector<u32> v;
+      if (host_off) {
+        b = host_off[op];
+        e = host_off[op + 1];
+        v.assign(host_vals + b, host_vals + e);
+      } else {
+        u64 be[2];
+        CK(cudaMemcpy(be, tr.offsets + op, 16, cudaMemcpyDeviceToHost));
+        b = be[0];
+        e = be[1];
+        v.resize(e - b);
+        CK(cudaMemcpy(v.data(), tr.vals + b, (e - b) * 4, cudaMemcpyDeviceToHost));
+      }
+      u64 mx = 0;
+      for (u32 x : v) mx = std::max<u64>(mx, x);
+      pbh_status st = grow_universe(h->H, h->stream, mx + 1);
+      if (st) return st;
+      begin = op;
+      CK(cudaMemsetAsync(&h->d_ks->status, 0, 4, h->stream));
+      continue;
+    }
+    if (n_out) *n_out = ks.n_out;
+    if (failed_op) *failed_op = ks.failed_op;
+    if (wall_ms) *wall_ms = ms_total;
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "op %llu: ", (unsigned long long)ks.failed_op);
+    return set_err(ks.status == 1 ? PBH_EMPTY : ks.status == 3 ? PBH_INVARIANT : PBH_PRECONDITION,
+                   std::string(buf) + detail_message(ks.detail));
+  }
+  if (n_out) *n_out = h->h_ks->n_out;
+  if (failed_op) *failed_op = ~0ull;
+  if (wall_ms) *wall_ms = ms_total;
+  return PBH_OK;
+}
+
+// Run a small host-side trace through the staging buffers.
+pbh_status exec_host(pbh_heap* h, u64 n_ops, const u8* kinds, const u64* off, const u32* vals,
+                     const u64* prios, u32* out_v, u64* out_p, u64* n_out, u64* failed_op,
+                     u32 internal, double* wall_ms) {
+  const u64 n_el = off[n_ops];
+  u64 n_x = 0;
+  u64 max_batch = 0;
+  for (u64 i = 0; i < n_ops; ++i) {
+    n_x += kinds[i] == 'E' || kinds[i] == 'F';
+    if (kinds[i] == 'B') max_batch = std::max<u64>(max_batch, off[i + 1] - off[i]);
+  }
+  pbh_status st;
+  if ((st = ensure_batch(h, std::min<u64>(max_batch, h->d)))) return st;
+  if ((st = ensure_staging(h, n_ops, n_el, n_x))) return st;
+  CK(cudaMemcpyAsync(h->d_kinds, kinds, n_ops, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->d_off, off, (n_ops + 1) * 8, cudaMemcpyHostToDevice, h->stream));
+  if (n_el) {
+    CK(cudaMemcpyAsync(h->d_vals, vals, n_el * 4, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->d_prios, prios, n_el * 8, cudaMemcpyHostToDevice, h->stream));
+  }
+  pbh_trace_dev tr{h->d_kinds, h->d_off, h->d_vals, h->d_prios};
+  u64 got = 0;
+  pbh_status rs = exec_trace(h, n_ops, tr, h->d_ov, h->d_op, &got, failed_op, internal, wall_ms,
+                             kinds, off, vals);
+  if (n_out) *n_out = got;
+  if (got && out_v) {
+    CK(cudaMemcpyAsync(out_v, h->d_ov, got * 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(out_p, h->d_op, got * 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  }
+  return rs;
+}
+
+pbh_status single_op(pbh_heap* h, u8 kind, const u32* vals, const u64* prios, u64 n, u32* ov,
+                     u64* op) {
+  u64 off[2] = {0, n};
+  u64 got = 0;
+  pbh_status st = exec_host(h, 1, &kind, off, vals, prios, ov, op, &got, nullptr, 1, nullptr);
+  if (st == PBH_OK && (kind == 'E' || kind == 'F') && got != 1)
+    return set_err(PBH_INVARIANT, "extract produced no element");
+  return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pbh_last_error(void) { return g_last_error.c_str(); }
+const char* pbh_version(void) { return "pbh-b200 0.1 (sm_100a)"; }
+
+pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int debug_checks,
+                           pbh_heap** out) {
+  if (!out) return set_err(PBH_PRECONDITION, "null output handle");
+  *out = nullptr;
+  if (d == 0) return set_err(PBH_PRECONDITION, "bucket heap: d must be positive");
+  if (d > (1ull << 40)) return set_err(PBH_PRECONDITION, "bucket heap: d too large");
+  CK(cudaSetDevice(device));
+  pbh_heap* h = new pbh_heap();
+  h->device = device;
+  h->d = d;
+  h->nt = pick_nt(d);
+  if (key_universe == 0) key_universe = 1 << 16;
+  const u32 cap0 = pick_cap0(d);
+  const u32 bc = (u32)pow2_at_least(std::max<u64>(std::min<u64>(d, 4096), 2));
+  auto fail = [&](pbh_status s) {
+    h->H.free_all();
+    delete h;
+    return s;
+  };
+  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(set_err(PBH_CUDA, "stream create failed"));
+  pbh_status st = init_heap(h->H, d, cap0, bc, h->nt, key_universe, debug_checks, 2, nullptr);
+  if (st) return fail(st);
+  h->layout = make_layout(h->nt, cap0, h->H.bc, h->H.hd.d, false);
+  if (cudaMalloc(&h->d_ks, sizeof(pbh_kstatus)) != cudaSuccess ||
+      cudaMallocHost(&h->h_ks, sizeof(pbh_kstatus)) != cudaSuccess)
+    return fail(set_err(PBH_OOM, "status block allocation failed"));
+  cudaEventCreate(&h->ev0);
+  cudaEventCreate(&h->ev1);
+  *out = h;
+  return PBH_OK;
+}
+
+pbh_status pbh_heap_destroy(pbh_heap* h) {
+  if (!h) return PBH_OK;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  h->H.free_all();
+  cudaFree(h->d_ks);
+  cudaFreeHost(h->h_ks);
+  cudaFree(h->d_kinds);
+  cudaFree(h->d_off);
+  cudaFree(h->d_vals);
+  cudaFree(h->d_prios);
+  cudaFree(h->d_ov);
+  cudaFree(h->d_op);
+  cudaEventDestroy(h->ev0);
+  cudaEventDestroy(h->ev1);
+  cudaStreamDestroy(h->stream);
+  delete h;
+  return PBH_OK;
+}
+
+pbh_status pbh_heap_update(pbh_heap* h, uint32_t value, uint64_t priority) {
+  if (!h) return set_err(PBH_PRECONDITION, "null heap");
+  cudaSetDevice(h->device);
+  return single_op(h, 'U', &value, &priority, 1, nullptr, nullptr);
+}
+
+pbh_status pbh_heap_bulk_update(pbh_heap* h, const uint32_t* values, const uint64_t* priorities,
+                                uint64_t n) {
+  if (!h) return set_err(PBH_PRECONDITION, "null heap");
+  if (n == 0) return set_err(PBH_PRECONDITION, "bulk_update: empty batch");
+  if (n > h->d) return set_err(PBH_PRECONDITION, "bulk_update: batch larger than d");
+  for (u64 i = 1; i < n; ++i)
+    if (values[i - 1] >= values[i])
+      return set_err(PBH_PRECONDITION, "bulk_update: batch must be value-sorted with unique values");
+  cudaSetDevice(h->device);
+  return single_op(h, 'B', values, priorities, n, nullptr, nullptr);
+}
+
+pbh_status pbh_heap_extract_min(pbh_heap* h, uint32_t* value, uint64_t* priority) {
+  if (!h) return set_err(PBH_PRECONDITION, "null heap");
+  cudaSetDevice(h->device);
+  u32 v = 0;
+  u64 p = 0;
+  pbh_status st = single_op(h, 'E', nullptr, nullptr, 0, &v, &p);
+  if (st == PBH_EMPTY) return set_err(PBH_EMPTY, "extract_min: heap is empty");
+  if (st == PBH_OK) {
+    if (value) *value = v;
+    if (priority) *priority = p;
+  }
+  return st;
+}
+
+pbh_status pbh_heap_find_min(pbh_heap* h, uint32_t* value, uint64_t* priority) {
+  if (!h) return set_err(PBH_PRECONDITION, "null heap");
+  cudaSetDevice(h->device);
+  u32 v = 0;
+  u64 p = 0;
+  pbh_status st = single_op(h, 'F', nullptr, nullptr, 0, &v, &p);
+  if (st == PBH_EMPTY) return set_err(PBH_EMPTY, "find_min: heap is empty");
+  if (st == PBH_OK) {
+    if (value) *value = v;
+    if (priority) *priority = p;
+  }
+  return st;
+}
+
+pbh_status pbh_heap_delete(pbh_heap* h, uint32_t value) {
+  if (!h) return set_err(PBH_PRECONDITION, "null heap");
+  cudaSetDevice(h->device);
+  const u64 dummy = 0;
+  return single_op(h, 'D', &value, &dummy, 1, nullptr, nullptr);
+}
+
+pbh_status pbh_heap_live_size(pbh_heap* h, int64_t* n) {
+  if (!h || !n) return set_err(PBH_PRECONDITION, "null argument");
+  cudaSetDevice(h->device);
+  CK(cudaMemcpyAsync(n, &h->H.dev->live, 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return PBH_OK;
+}
+
+pbh_status pbh_heap_drain(pbh_heap* h) {
+  if (!h) return set_err(PBH_PRECONDITION, "null heap");
+  cudaSetDevice(h->device);
+  return single_op(h, kOpDrain, nullptr, nullptr, 0, nullptr, nullptr);
+}
+
+pbh_status pbh_heap_metrics(pbh_heap* h, uint64_t* ops, uint64_t* resolves, uint64_t* touches,
+                            uint32_t* n_levels) {
+  if (!h) return set_err(PBH_PRECONDITION, "null heap");
+  cudaSetDevice(h->device);
+  pbh_heap_dev hd;
+  CK(cudaMemcpyAsync(&hd, h->H.dev, sizeof(hd), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  // levels that ever held content (BucketHeap::allocated_levels)
+  u32 used = 1;
+  for (u32 i = 0; i < hd.n_levels; ++i)
+    if (hd.resolves[i] || hd.touches[i]) used = i + 1;
+  if (ops) *ops = hd.ops;
+  for (u32 i = 0; i < PBH_MAX_LEVELS; ++i) {
+    if (resolves) resolves[i] = i < used ? hd.resolves[i] : 0;
+    if (touches) touches[i] = i < used ? hd.touches[i] : 0;
+  }
+  if (n_levels) *n_levels = used;
+  return PBH_OK;
+}
+
+pbh_status pbh_heap_check_invariants(pbh_heap* h, uint64_t* n_violations) {
+  if (!h || !n_violations) return set_err(PBH_PRECONDITION, "null argument");
+  cudaSetDevice(h->device);
+  pbh_heap_dev hd;
+  CK(cudaMemcpyAsync(&hd, h->H.dev, sizeof(hd), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  std::vector<pbh_idx_entry> idx(hd.universe);
+  CK(cudaMemcpy(idx.data(), hd.idx, hd.universe * sizeof(pbh_idx_entry), cudaMemcpyDeviceToHost));
+  u64 bad = 0;
+  std::string first;
+  auto complain = [&](const std::string& m) {
+    if (!bad) first = m;
+    ++bad;
+  };
+  auto less = [](u64 pa, u32 ka, u64 pb, u32 kb) { return pa < pb || (pa == pb && ka < kb); };
+  u64 valid_entries = 0;
+  bool have_prev = false;
+  u64 prev_p = 0;
+  u32 prev_k = 0;  // max of all buckets so far
+  for (u32 i = 0; i < hd.n_levels; ++i) {
+    const pbh_level_state& t = hd.st[i];
+    const pbh_level_bufs& b = hd.lv[i];
+    const u32 cap = i == 0 ? hd.cap0 : b.cap_b;
+    if (t.b_size > cap) complain("level " + std::to_string(i) + ": bucket over capacity");
+    std::vector<u32> bk(t.b_size), sk(t.s_size);
+    std::vector<u64> bp(t.b_size), sp(t.s_size);
+    if (t.b_size) {
+      CK(cudaMemcpy(bk.data(), b.bk[t.b_sel] + t.b_head, t.b_size * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(bp.data(), b.bp[t.b_sel] + t.b_head, t.b_size * 8, cudaMemcpyDeviceToHost));
+    }
+    if (t.s_size) {
+      CK(cudaMemcpy(sk.data(), b.sk[t.s_sel] + t.s_head, t.s_size * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(sp.data(), b.sp[t.s_sel] + t.s_head, t.s_size * 8, cudaMemcpyDeviceToHost));
+    }
+    for (u32 j = 1; j < t.b_size; ++j)
+      if (!less(bp[j - 1], bk[j - 1], bp[j], bk[j])) {
+        complain("level " + std::to_string(i) + ": bucket not strictly sorted");
+        break;
+      }
+    for (u32 j = 1; j < t.s_size; ++j)
+      if (!less(sp[j - 1], sk[j - 1], sp[j], sk[j])) {
+        complain("level " + std::to_string(i) + ": signal buffer not strictly sorted");
+        break;
+      }
+    for (u32 j = 0; j < t.b_size; ++j) {
+      const bool adm = t.spl_inf || bp[j] < t.spl_p || (bp[j] == t.spl_p && bk[j] <= t.spl_k);
+      if (!adm) {
+        complain("level " + std::to_string(i) + ": bucket element above splitter");
+        break;
+      }
+    }
+    // everything at this level must lie above every shallower bucket
+    if (have_prev) {
+      if (t.b_size && !less(prev_p, prev_k, bp[0], bk[0]))
+        complain("level " + std::to_string(i) + ": bucket overlaps shallower bucket");
+      if (t.s_size && !less(prev_p, prev_k, sp[0], sk[0]))
+        complain("level " + std::to_string(i) + ": signal overlaps shallower bucket");
+    }
+    if (t.b_size) {
+      have_prev = true;
+      prev_p = bp[t.b_size - 1];
+      prev_k = bk[t.b_size - 1];
+    }
+    auto valid = [&](u32 k, u64 p) {
+      return k < hd.universe && idx[k].state == PBH_ST_LIVE && idx[k].prio == p;
+    };
+    for (u32 j = 0; j < t.b_size; ++j) {
+      const bool ok = valid(bk[j], bp[j]);
+      valid_entries += ok;
+      if (i == 0 && !ok) complain("level 0: stale entry in B_0");
+    }
+    for (u32 j = 0; j < t.s_size; ++j) valid_entries += valid(sk[j], sp[j]);
+  }
+  u64 live_idx = 0;
+  for (const auto& e : idx) live_idx += e.state == PBH_ST_LIVE;
+  if ((i64)live_idx != hd.live)
+    complain("live_size " + std::to_string(hd.live) + " != live index entries " +
+             std::to_string(live_idx));
+  if (valid_entries != live_idx)
+    complain("valid stored entries " + std::to_string(valid_entries) + " != live values " +
+             std::to_string(live_idx));
+  *n_violations = bad;
+  if (bad) g_last_error = first;
+  return PBH_OK;
+}
+
+pbh_status pbh_heap_run_trace(pbh_heap* h, uint64_t n_ops, const uint8_t* kinds,
+                              const uint64_t* offsets, const uint32_t* values,
+                              const uint64_t* priorities, uint32_t* out_values,
+                              uint64_t* out_priorities, uint64_t* n_out, uint64_t* failed_op,
+                              double* wall_ms) {
+  if (!h) return set_err(PBH_PRECONDITION, "null heap");
+  if (failed_op) *failed_op = ~0ull;
+  if (n_out) *n_out = 0;
+  if (wall_ms) *wall_ms = 0;
+  cudaSetDevice(h->device);
+  // host-side structural validation of the flat trace
+  for (u64 i = 0; i < n_ops; ++i) {
+    const u64 len = offsets[i + 1] - offsets[i];
+    const u8 k = kinds[i];
+    const bool ok = (k == 'U' && len == 1) || (k == 'B') || (k == 'E' && len == 0) ||
+                    (k == 'D' && len == 1);
+    if (!ok || offsets[i + 1] < offsets[i]) {
+      if (failed_op) *failed_op = i;
+      return set_err(PBH_TRACE, "op " + std::to_string(i) + ": malformed op");
+    }
+  }
+  pbh_status st = exec_host(h, n_ops, kinds, offsets, values, priorities, out_values,
+                            out_priorities, n_out, failed_op, 0, wall_ms);
+  if (st == PBH_EMPTY || st == PBH_PRECONDITION) {
+    return set_err(PBH_TRACE, g_last_error);  // TraceError(op_index) (engine.cpp:213-219)
+  }
+  if (st) return st;
+  // Engine::run_trace drains before returning (engine.cpp:221)
+  double dms = 0;
+  u8 k = kOpDrain;
+  u64 off[2] = {0, 0};
+  st = exec_host(h, 1, &k, off, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 1, &dms);
+  if (wall_ms) *wall_ms += dms;
+  return st;
+}
+
+pbh_status pbh_heap_run_trace_device(pbh_heap* h, uint64_t n_ops, const uint8_t* d_kinds,
+                                     const uint64_t* d_offsets, const uint32_t* d_values,
+                                     const uint64_t* d_priorities, uint32_t* d_out_values,
+                                     uint64_t* d_out_priorities, uint64_t* n_out,
+                                     uint64_t* failed_op, double* wall_ms) {
+  if (!h) return set_err(PBH_PRECONDITION, "null heap");
+  cudaSetDevice(h->device);
+  if (failed_op) *failed_op = ~0ull;
+  pbh_trace_dev tr{d_kinds, d_offsets, d_values, d_priorities};
+  // batch scratch must cover the largest batch: bounded by d
+  pbh_status st = ensure_batch(h, std::min<u64>(h->d, 1ull << 26));
+  if (st) return st;
+  st = exec_trace(h, n_ops, tr, d_out_values, d_out_priorities, n_out, failed_op, 0, wall_ms,
+                  nullptr, nullptr, nullptr);
+  if (st == PBH_EMPTY || st == PBH_PRECONDITION) return set_err(PBH_TRACE, g_last_error);
+  if (st) return st;
+  double dms = 0;
+  u8 k = kOpDrain;
+  u64 off[2] = {0, 0};
+  st = exec_host(h, 1, &k, off, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 1, &dms);
+  if (wall_ms) *wall_ms += dms;
+  return st;
+}
+
+// =========================================================================
+// SSSP
+// =========================================================================
+struct pbh_sssp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  u32 V = 0;
+  u64 E = 0;
+  u64* d_off = nullptr;
+  u32* d_tgt = nullptr;
+  u32* d_w = nullptr;
+  u32 max_deg = 0;
+  u64 d = 0;
+  int nt = 32;
+  u32 cap0 = 0;
+  u64 max_sources = 0;
+  SmLayout layout{};
+  std::vector<DevHeap> heaps;
+  pbh_heap_dev* d_heaps = nullptr;
+  SsspState* d_sst = nullptr;
+  u64* d_dist = nullptr;
+  u32* d_settled = nullptr;
+  u32* d_parent = nullptr;
+  u32* d_src = nullptr;
+  u64 n_last = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+pbh_status ctx_alloc(pbh_sssp_ctx* c, void** p, size_t bytes) {
+  CK(cudaMalloc(p, bytes ? bytes : 16));
+  c->allocs.push_back(*p);
+  return PBH_OK;
+}
+
+void ctx_free(pbh_sssp_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& H : c->heaps) H.free_all();
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+}  // namespace
+
+pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_t max_sources,
+                               pbh_sssp_ctx** out) {
+  if (!g || !out || max_sources == 0) return set_err(PBH_PRECONDITION, "bad arguments");
+  *out = nullptr;
+  CK(cudaSetDevice(device));
+  pbh_sssp_ctx* c = new pbh_sssp_ctx();
+  c->device = device;
+  c->V = g->vertex_count;
+  c->E = g->edge_count;
+  c->max_sources = max_sources;
+  auto fail = [&](pbh_status s) {
+    ctx_free(c);
+    return s;
+  };
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(set_err(PBH_CUDA, "stream create failed"));
+  cudaEventCreate(&c->ev0);
+  cudaEventCreate(&c->ev1);
+  pbh_status st;
+  if ((st = ctx_alloc(c, (void**)&c->d_off, ((u64)c->V + 1) * 8))) return fail(st);
+  if ((st = ctx_alloc(c, (void**)&c->d_tgt, c->E * 4))) return fail(st);
+  if ((st = ctx_alloc(c, (void**)&c->d_w, c->E * 4))) return fail(st);
+  if (cudaMemcpyAsync(c->d_off, g->offsets, ((u64)c->V + 1) * 8, cudaMemcpyHostToDevice, c->stream) ||
+      (c->E && cudaMemcpyAsync(c->d_tgt, g->targets, c->E * 4, cudaMemcpyHostToDevice, c->stream)) ||
+      (c->E && cudaMemcpyAsync(c->d_w, g->weights, c->E * 4, cudaMemcpyHostToDevice, c->stream)))
+    return fail(set_err(PBH_CUDA, "CSR upload failed"));
+  // max out-degree on the device (graphs.cpp:47-53)
+  unsigned long long* d_md = nullptr;
+  if ((st = ctx_alloc(c, (void**)&d_md, 8))) return fail(st);
+  cudaMemsetAsync(d_md, 0, 8, c->stream);
+  k_max_degree<<<std::max<u32>(1, std::min<u32>(1184, (c->V + 255) / 256)), 256, 0, c->stream>>>(
+      c->d_off, c->V, d_md);
+  unsigned long long md = 0;
+  cudaMemcpyAsync(&md, d_md, 8, cudaMemcpyDeviceToHost, c->stream);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return fail(set_err(PBH_CUDA, "max-degree kernel failed"));
+  c->max_deg = (u32)md;
+  c->d = d ? d : std::max<u64>(1, md);  // sssp.cpp:24-26
+  c->d = std::min<u64>(c->d, std::max<u64>(1, md ? md : 1));  // batches never exceed a row
+  c->nt = pick_nt(std::max<u64>(c->d, std::min<u64>(md, 1024)));
+  c->cap0 = pick_cap0(c->d);
+  const u32 bc = (u32)pow2_at_least(std::max<u64>(c->d, 2));
+  c->layout = make_layout(c->nt, c->cap0, bc, (u32)c->d, true);
+  if ((st = ctx_alloc(c, (void**)&c->d_heaps, max_sources * sizeof(pbh_heap_dev)))) return fail(st);
+  if ((st = ctx_alloc(c, (void**)&c->d_sst, max_sources * sizeof(SsspState)))) return fail(st);
+  if ((st = ctx_alloc(c, (void**)&c->d_dist, max_sources * c->V * 8))) return fail(st);
+  if ((st = ctx_alloc(c, (void**)&c->d_settled, max_sources * c->V * 4))) return fail(st);
+  if ((st = ctx_alloc(c, (void**)&c->d_parent, max_sources * c->V * 4))) return fail(st);
+  if ((st = ctx_alloc(c, (void**)&c->d_src, max_sources * 4))) return fail(st);
+  c->heaps.resize(max_sources);
+  // initial levels: enough for a few rows of relaxations
+  u32 nlev = 2;
+  while (nlev < 8 && ((u64)c->cap0 << (2 * (nlev - 1))) < 8ull * (c->max_deg + 1)) ++nlev;
+  for (u64 i = 0; i < max_sources; ++i) {
+    st = init_heap(c->heaps[i], c->d, c->cap0, bc, c->nt, std::max<u32>(c->V, 1), 0, nlev,
+                   c->d_heaps + i);
+    if (st) return fail(st);
+  }
+  *out = c;
+  return PBH_OK;
+}
+
+namespace {
+
+// Reset slot state (heap header, index, outputs) for a new solve.
+pbh_status ctx_reset(pbh_sssp_ctx* c, u64 n) {
+  for (u64 i = 0; i < n; ++i) {
+    DevHeap& H = c->heaps[i];
+    for (u32 l = 0; l < PBH_MAX_LEVELS; ++l) {
+      H.hd.st[l] = pbh_level_state{};
+      H.hd.st[l].spl_inf = 1;
+      H.hd.resolves[l] = 0;
+      H.hd.touches[l] = 0;
+    }
+    H.hd.live = 0;
+    H.hd.ops = 0;
+    CK(cudaMemcpyAsync(H.dev, &H.hd, sizeof(pbh_heap_dev), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(H.hd.idx, 0xff, (u64)c->V * sizeof(pbh_idx_entry), c->stream));
+  }
+  CK(cudaMemsetAsync(c->d_sst, 0, n * sizeof(SsspState), c->stream));
+  CK(cudaMemsetAsync(c->d_dist, 0xff, n * c->V * 8, c->stream));
+  return PBH_OK;
+}
+
+}  // namespace
+
+pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n_sources,
+                            int dag_mode, double* device_ms) {
+  if (!c) return set_err(PBH_PRECONDITION, "null context");
+  if (n_sources == 0 || n_sources > c->max_sources)
+    return set_err(PBH_PRECONDITION, "n_sources out of range");
+  for (u64 i = 0; i < n_sources; ++i)
+    if (sources[i] >= c->V) return set_err(PBH_PRECONDITION, "par_dijkstra: source out of range");
+  CK(cudaSetDevice(c->device));
+  pbh_status st = ctx_reset(c, n_sources);
+  if (st) return st;
+  CK(cudaMemcpyAsync(c->d_src, sources, n_sources * 4, cudaMemcpyHostToDevice, c->stream));
+  double ms_total = 0;
+  std::vector<SsspState> hs(n_sources);
+  for (int guard = 0; guard < 256; ++guard) {
+    CK(cudaEventRecord(c->ev0, c->stream));
+    CK(launch_sssp_nt(c->nt, c->layout, c->stream, (u32)n_sources, c->d_heaps, c->d_off, c->d_tgt,
+                      c->d_w, c->V, c->d_src, c->d_dist, c->d_settled, c->d_sst, dag_mode ? 1 : 0,
+                      c->max_deg));
+    CK(cudaEventRecord(c->ev1, c->stream));
+    CK(cudaMemcpyAsync(hs.data(), c->d_sst, n_sources * sizeof(SsspState), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    ms_total += ms;
+    bool again = false;
+    for (u64 i = 0; i < n_sources; ++i) {
+      if (hs[i].status == 7) {
+        st = grow_levels(c->heaps[i], c->stream);
+        if (st) return st;
+        again = true;
+      } else if (hs[i].status != 0) {
+        return set_err(hs[i].status == 3 ? PBH_INVARIANT : PBH_PRECONDITION,
+                       std::string("sssp source slot ") + std::to_string(i) + ": " +
+                           detail_message(hs[i].detail));
+      }
+    }
+    if (!again) break;
+    // clear NEED_GROW status so the kernel resumes
+    for (u64 i = 0; i < n_sources; ++i)
+      if (hs[i].status == 7) CK(cudaMemsetAsync(&c->d_sst[i].status, 0, 4, c->stream));
+  }
+  for (u64 i = 0; i < n_sources; ++i) {
+    k_finalize_parent<<<std::max<u32>(1, std::min<u32>(1184, (c->V + 255) / 256)), 256, 0,
+                        c->stream>>>(c->heaps[i].hd.idx, c->V, c->d_parent + i * c->V);
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
+  c->n_last = n_sources;
+  if (device_ms) *device_ms = ms_total;
+  return PBH_OK;
+}
+
+pbh_status pbh_sssp_ctx_fetch(pbh_sssp_ctx* c, uint64_t slot, uint64_t* dist, uint32_t* parent,
+                              uint32_t* settled, uint64_t* n_settled, uint64_t* rounds,
+                              uint64_t* ops) {
+  if (!c || slot >= c->n_last) return set_err(PBH_PRECONDITION, "bad slot");
+  CK(cudaSetDevice(c->device));
+  SsspState s;
+  CK(cudaMemcpyAsync(&s, c->d_sst + slot, sizeof s, cudaMemcpyDeviceToHost, c->stream));
+  if (dist) CK(cudaMemcpyAsync(dist, c->d_dist + slot * c->V, (u64)c->V * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (parent) CK(cudaMemcpyAsync(parent, c->d_parent + slot * c->V, (u64)c->V * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (settled && s.n_settled)
+    CK(cudaMemcpy(settled, c->d_settled + slot * c->V, s.n_settled * 4, cudaMemcpyDeviceToHost));
+  if (n_settled) *n_settled = s.n_settled;
+  if (rounds) *rounds = s.rounds;
+  if (ops) {
+    u64 o = 0;
+    CK(cudaMemcpy(&o, &c->heaps[slot].dev->ops, 8, cudaMemcpyDeviceToHost));
+    *ops = o;
+  }
+  return PBH_OK;
+}
+
+pbh_status pbh_sssp_ctx_destroy(pbh_sssp_ctx* c) {
+  ctx_free(c);
+  return PBH_OK;
+}
+
+pbh_status pbh_sssp(const pbh_csr* g, uint32_t source, uint64_t d, int dag_mode, int device,
+                    uint64_t* dist, uint32_t* parent, uint32_t* settled, uint64_t* n_settled,
+                    uint64_t* rounds, uint64_t* ops) {
+  if (!g) return set_err(PBH_PRECONDITION, "null graph");
+  if (source >= g->vertex_count) return set_err(PBH_PRECONDITION, "par_dijkstra: source out of range");
+  pbh_sssp_ctx* c = nullptr;
+  pbh_status st = pbh_sssp_ctx_create(g, d, device, 1, &c);
+  if (st) return st;
+  st = pbh_sssp_ctx_run(c, &source, 1, dag_mode, nullptr);
+  if (!st) st = pbh_sssp_ctx_fetch(c, 0, dist, parent, settled, n_settled, rounds, ops);
+  pbh_sssp_ctx_destroy(c);
+  return st;
+}
+
+pbh_status pbh_sssp_multi(const pbh_csr* g, const uint32_t* sources, uint64_t n_sources,
+                          uint64_t d, const int* devices, int n_devices, uint64_t* dist,
+                          uint32_t* parent) {
+  if (!g || !sources || !dist || n_devices <= 0) return set_err(PBH_PRECONDITION, "bad arguments");
+  std::vector<pbh_status> res(n_devices, PBH_OK);
+  std::vector<std::string> msg(n_devices);
+  std::vector<std::thread> th;
+  const u64 per = (n_sources + n_devices - 1) / n_devices;
+  for (int r = 0; r < n_devices; ++r) {
+    const u64 b = std::min<u64>(n_sources, r * per), e = std::min<u64>(n_sources, b + per);
+    if (b >= e) continue;
+    th.emplace_back([&, r, b, e] {
+      pbh_sssp_ctx* c = nullptr;
+      pbh_status st = pbh_sssp_ctx_create(g, d, devices[r], e - b, &c);
+      if (!st) st = pbh_sssp_ctx_run(c, sources + b, e - b, 0, nullptr);
+      for (u64 i = b; !st && i < e; ++i)
+        st = pbh_sssp_ctx_fetch(c, i - b, dist + i * g->vertex_count,
+                                parent ? parent + i * g->vertex_count : nullptr, nullptr, nullptr,
+                                nullptr, nullptr);
+      if (c) pbh_sssp_ctx_destroy(c);
+      res[r] = st;
+      if (st) msg[r] = g_last_error;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int r = 0; r < n_devices; ++r)
+    if (res[r]) return set_err(res[r], msg[r]);
+  return PBH_OK;
+}
+
+uint64_t pbh_distance_checksum(const uint64_t* dist, uint64_t n) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (uint64_t i = 0; i < n; ++i)
+    for (int b = 0; b < 8; ++b) {
+      h ^= (dist[i] >> (8 * b)) & 0xff;
+      h *= 0x100000001b3ull;
+    }
+  return h;
+}
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+// Device-resident heap layout shared by the kernels and the host runtime.
+// Plain C layout (no torch types): everything below lives in HBM.
+#pragma once
+#include <stdint.h>
+
+#define PBH_MAX_LEVELS 24
+
+// Per-key position index entry (16 B, one sector-aligned load):
+//   prio   current priority of the key's single valid copy
+//   state  PBH_ST_ABSENT (never inserted), PBH_ST_LIVE, PBH_ST_DEAD
+//   parent SSSP predecessor (unused by the plain heap)
+// A memset to 0xFF is the initial state (absent, prio = kInfDist).
+#define PBH_ST_ABSENT 0xFFFFFFFFu
+#define PBH_ST_LIVE 1u
+#define PBH_ST_DEAD 2u
+
+typedef struct __attribute__((aligned(16))) {
+  uint64_t prio;
+  uint32_t state;
+  uint32_t parent;
+} pbh_idx_entry;
+
+// Mutable per-level state. B_i = bucket run bk/bp[b_sel][b_head, b_head+b_size),
+// S_i = signal run sk/sp[s_sel][s_head, s_head+s_size). Both (prio, key)-sorted.
+typedef struct {
+  uint32_t b_sel, s_sel;
+  uint32_t b_head, b_size;
+  uint32_t s_head, s_size;
+  uint32_t spl_inf, spl_k;
+  uint64_t spl_p;
+} pbh_level_state;
+
+// Immutable per-level buffers (ping-pong pairs).
+typedef struct {
+  uint32_t* bk[2];
+  uint64_t* bp[2];
+  uint32_t* sk[2];
+  uint64_t* sp[2];
+  uint32_t cap_b;  // bucket capacity (elements)
+  uint32_t buf_s;  // signal buffer capacity (elements, 2x the signal capacity)
+  uint32_t pad[2];
+} pbh_level_bufs;
+
+typedef struct {
+  pbh_level_bufs lv[PBH_MAX_LEVELS];
+  pbh_level_state st[PBH_MAX_LEVELS];
+  pbh_idx_entry* idx;
+  uint64_t universe;
+  uint32_t n_levels;  // allocated levels
+  uint32_t d;         // batch bound
+  uint32_t cap0;      // B_0 capacity
+  uint32_t debug_checks;
+  int64_t live;
+  uint64_t ops;
+  uint64_t resolves[PBH_MAX_LEVELS];
+  uint64_t touches[PBH_MAX_LEVELS];
+  // level-0 scratch in HBM (used when B_0 does not fit in shared memory):
+  // batch keys/prios (d), push list (d), B_0 removal flags (cap0)
+  uint32_t* g_bk;
+  uint64_t* g_bp;
+  uint32_t* g_pk;
+  uint64_t* g_pp;
+  uint8_t* g_rm;
+  // SSSP relaxation collection (d + 1024 entries)
+  uint32_t* g_ck;
+  uint64_t* g_cp;
+  uint64_t* g_co;
+  uint32_t* g_cs;
+} pbh_heap_dev;
+
+// Op stream (trace_format.hpp:16-33) in device memory.
+typedef struct {
+  const uint8_t* kinds;     // 'U','B','E','D'
+  const uint64_t* offsets;  // n_ops + 1
+  const uint32_t* vals;
+  const uint64_t* prios;
+} pbh_trace_dev;
+
+// Kernel status block (device memory, read back by the host).
+typedef struct {
+  uint32_t status;      // pbh_status
+  uint32_t detail;      // PBH_ERR_*
+  uint64_t ops_done;    // ops fully applied in this launch
+  uint64_t n_out;       // extracted elements written (cumulative)
+  uint64_t failed_op;   // op index of the failure
+  uint64_t aux;         // detail payload (value, level, ...)
+  uint64_t pad[3];
+} pbh_kstatus;
+
+// error details (mapped to the reference's messages on the host)
+#define PBH_ERR_NONE 0
+#define PBH_ERR_EMPTY_HEAP 1       // bucket_heap.cpp:68-69
+#define PBH_ERR_EMPTY_BATCH 2      // bucket_heap.cpp:129
+#define PBH_ERR_BATCH_TOO_BIG 3    // bucket_heap.cpp:130
+#define PBH_ERR_UNSORTED 4         // bucket_heap.cpp:133-135
+#define PBH_ERR_REINSERT 5         // bucket_heap.cpp:55-58
+#define PBH_ERR_INCREASE 6         // bucket_heap.cpp:60-62
+#define PBH_ERR_NEED_GROW 7        // internal: allocate a deeper level and resume
+#define PBH_ERR_INVARIANT 8        // internal invariant broken
+#define PBH_ERR_OVERFLOW 9         // sssp.cpp:13-17 distance overflow
+#define PBH_ERR_KEY_RANGE 10       // key >= universe (host grows the index first)
+#define PBH_ERR_BAD_OP 11          // unknown op kind

@@ -1,0 +1,183 @@
+"""Host-side mirror of the reference SSSP API (/root/reference/proj/include/pbh/sssp.hpp:13-48)
+over the pbh-b200 C-ABI: ``par_dijkstra`` runs as one persistent CTA per
+source on the B200; ``par_dijkstra_multi`` shards independent sources.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import raise_for
+
+K_INF_DIST = (1 << 64) - 1  # sssp.hpp:16
+
+
+@dataclass
+class CsrGraph:
+    """graphs.hpp:11-20: offsets u64[V+1], targets u32[E], weights u32[E]."""
+    vertex_count: int
+    offsets: np.ndarray
+    targets: np.ndarray
+    weights: np.ndarray
+
+    @property
+    def edge_count(self):
+        return len(self.targets)
+
+    @staticmethod
+    def of(g):
+        """Adopt any object with V/off/tgt/w or vertex_count/offsets/targets/weights."""
+        if isinstance(g, CsrGraph):
+            return g
+        if hasattr(g, "off"):
+            return CsrGraph(int(g.V), g.off, g.tgt, g.w)
+        return CsrGraph(int(g.vertex_count), g.offsets, g.targets, g.weights)
+
+    def c_struct(self):
+        self._off = np.ascontiguousarray(self.offsets, dtype=np.uint64)
+        self._tgt = np.ascontiguousarray(self.targets if len(self.targets) else [0], dtype=np.uint32)
+        self._w = np.ascontiguousarray(self.weights if len(self.weights) else [1], dtype=np.uint32)
+        return _lib.Csr(self.vertex_count, len(self.targets),
+                        self._off.ctypes.data_as(_lib.U64P), self._tgt.ctypes.data_as(_lib.U32P),
+                        self._w.ctypes.data_as(_lib.U32P))
+
+
+@dataclass
+class SsspResult:
+    """sssp.hpp:18-23 plus ``parent`` (shortest-path tree; extension)."""
+    dist: np.ndarray
+    settled_order: np.ndarray
+    rounds: int
+    ops: int
+    parent: np.ndarray | None = None
+
+
+def par_dijkstra(g, source: int, d: int = 0, dag_mode: bool = False, device: int = 0) -> SsspResult:
+    """par_dijkstra (sssp.hpp:28-29; sssp.cpp:21-69). ``d == 0`` selects the
+    maximum out-degree (sssp.cpp:24-26)."""
+    g = CsrGraph.of(g)
+    cs = g.c_struct()
+    V = g.vertex_count
+    dist = np.zeros(max(V, 1), np.uint64)
+    parent = np.zeros(max(V, 1), np.uint32)
+    settled = np.zeros(max(V, 1), np.uint32)
+    ns, nr, ops = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    raise_for(_lib.lib().pbh_sssp(C.byref(cs), int(source), int(d), int(dag_mode), device,
+                                  dist.ctypes.data_as(_lib.U64P), parent.ctypes.data_as(_lib.U32P),
+                                  settled.ctypes.data_as(_lib.U32P), C.byref(ns), C.byref(nr),
+                                  C.byref(ops)))
+    return SsspResult(dist[:V], settled[:ns.value], nr.value, ops.value, parent[:V])
+
+
+def par_dijkstra_multi(g, sources, d: int = 0, devices=(0,)):
+    """Independent sources dealt contiguously over ``devices`` (BASELINE C5).
+    Returns (dist[n_sources, V], parent[n_sources, V])."""
+    g = CsrGraph.of(g)
+    cs = g.c_struct()
+    src = np.ascontiguousarray(sources, dtype=np.uint32)
+    devs = (C.c_int * len(devices))(*devices)
+    dist = np.zeros((len(src), g.vertex_count), np.uint64)
+    parent = np.zeros((len(src), g.vertex_count), np.uint32)
+    raise_for(_lib.lib().pbh_sssp_multi(C.byref(cs), src.ctypes.data_as(_lib.U32P), len(src), d,
+                                        devs, len(devices), dist.ctypes.data_as(_lib.U64P),
+                                        parent.ctypes.data_as(_lib.U32P)))
+    return dist, parent
+
+
+class SsspContext:
+    """Device-resident CSR for repeated solves (bench: inputs already in HBM)."""
+
+    def __init__(self, g, d: int = 0, device: int = 0, max_sources: int = 1):
+        self.g = CsrGraph.of(g)
+        cs = self.g.c_struct()
+        h = C.c_void_p()
+        raise_for(_lib.lib().pbh_sssp_ctx_create(C.byref(cs), d, device, max_sources, C.byref(h)))
+        self._h = h
+
+    def run(self, sources, dag_mode=False) -> float:
+        src = np.ascontiguousarray(sources, dtype=np.uint32)
+        ms = C.c_double()
+        raise_for(_lib.lib().pbh_sssp_ctx_run(self._h, src.ctypes.data_as(_lib.U32P), len(src),
+                                              int(dag_mode), C.byref(ms)))
+        return ms.value
+
+    def fetch(self, slot=0, settled=True) -> SsspResult:
+        V = self.g.vertex_count
+        dist = np.zeros(max(V, 1), np.uint64)
+        parent = np.zeros(max(V, 1), np.uint32)
+        st = np.zeros(max(V, 1), np.uint32) if settled else None
+        ns, nr, ops = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        raise_for(_lib.lib().pbh_sssp_ctx_fetch(
+            self._h, slot, dist.ctypes.data_as(_lib.U64P), parent.ctypes.data_as(_lib.U32P),
+            st.ctypes.data_as(_lib.U32P) if settled else None, C.byref(ns), C.byref(nr),
+            C.byref(ops)))
+        return SsspResult(dist[:V], st[:ns.value] if settled else None, nr.value, ops.value,
+                          parent[:V])
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().pbh_sssp_ctx_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+def distance_checksum(dist) -> int:
+    """sssp.cpp:174-183."""
+    d = np.ascontiguousarray(dist, dtype=np.uint64)
+    return int(_lib.lib().pbh_distance_checksum(d.ctypes.data_as(_lib.U64P), len(d)))
+
+
+def distances_to_csv(dist) -> str:
+    """sssp.cpp:159-172."""
+    out = ["vertex,dist"]
+    for v, x in enumerate(np.asarray(dist, dtype=np.uint64).tolist()):
+        out.append(f"{v},{'inf' if x == K_INF_DIST else x}")
+    return "\n".join(out) + "\n"
+
+
+def validate_parent_tree(g, source, dist, parent) -> str | None:
+    """Shortest-path-tree validator: for every reached v != s,
+    parent[v] has an edge to v with dist[v] == dist[parent] + w; the source is
+    its own parent; unreachable vertices have no parent. Returns None when
+    valid, else a message."""
+    g = CsrGraph.of(g)
+    off = np.asarray(g.offsets, np.uint64)
+    tgt = np.asarray(g.targets, np.uint32)
+    w = np.asarray(g.weights, np.uint64)
+    dist = np.asarray(dist, np.uint64)
+    parent = np.asarray(parent, np.uint32)
+    V = g.vertex_count
+    if parent[source] != source or dist[source] != 0:
+        return "source is not the tree root"
+    reached = dist != np.uint64(K_INF_DIST)
+    if np.any(parent[~reached] != 0xFFFFFFFF):
+        return "unreachable vertex has a parent"
+    vs = np.nonzero(reached)[0]
+    vs = vs[vs != source]
+    if len(vs) == 0:
+        return None
+    par = parent[vs].astype(np.int64)
+    if np.any(par >= V) or np.any(~reached[par]):
+        return "parent out of range or unreached"
+    # locate edge par -> v in the target-sorted row of par
+    lo = off[par].astype(np.int64)
+    hi = off[par + 1].astype(np.int64)
+    # vectorised binary search per row
+    a, b = lo.copy(), hi.copy()
+    for _ in range(64):
+        m = (a + b) // 2
+        go = (a < b) & (tgt[np.minimum(m, len(tgt) - 1)] < vs)
+        a = np.where(go, m + 1, a)
+        b = np.where(go | (a >= b), b, m)
+        if not np.any(a < b):
+            break
+    ok = (a < hi) & (tgt[np.minimum(a, len(tgt) - 1)] == vs)
+    if not np.all(ok):
+        return "parent edge missing"
+    if not np.all(dist[par] + w[a] == dist[vs]):
+        return "dist[v] != dist[parent] + w"
+    return None

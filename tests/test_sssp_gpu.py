@@ -1,0 +1,138 @@
+"""SSSP parity on the B200 through the C-ABI.
+
+Restates /root/reference/proj/tests/test_sssp.cpp and acceptance criterion 5
+(acceptance_main.cpp:140-181) against paper_1908_09378_b200.par_dijkstra:
+distances and settled order bit-exact vs the oracle's reference_dijkstra
+(sssp.cpp:71-97), op counts equal to par_dijkstra's, parent trees valid.
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def check(pbh, O, g, source=0, d=0, dag=False):
+    want = O.dijkstra(g, source, d)
+    got = pbh.par_dijkstra(g, source, d=d, dag_mode=dag)
+    assert np.array_equal(got.dist, want["dist"])
+    assert np.array_equal(got.settled_order, want["settled_order"])
+    assert got.rounds == want["rounds"]
+    assert got.ops == want["ops"]
+    assert pbh.validate_parent_tree(g, source, got.dist, got.parent) is None
+    return got
+
+
+def test_path_graph(pbh, O):
+    g = O.make_graph(3, [(0, 1, 1), (1, 2, 2)])
+    r = check(pbh, O, g)
+    assert r.dist.tolist() == [0, 1, 3]
+    assert r.settled_order.tolist() == [0, 1, 2]
+    assert r.rounds == 3
+
+
+def test_shortcut(pbh, O):
+    g = O.make_graph(3, [(0, 1, 5), (0, 2, 1), (2, 1, 1)])
+    assert check(pbh, O, g).dist.tolist() == [0, 2, 1]
+
+
+def test_single_vertex(pbh, O):
+    g = O.make_graph(1, [])
+    assert check(pbh, O, g).dist.tolist() == [0]
+
+
+def test_unreachable(pbh, O):
+    g = O.make_graph(4, [(0, 1, 2), (1, 2, 2)])
+    r = check(pbh, O, g)
+    assert r.dist[3] == pbh.K_INF_DIST
+    assert 3 not in r.settled_order.tolist()
+    assert len(r.settled_order) == 3
+    assert r.parent[3] == 0xFFFFFFFF
+
+
+def test_source_out_of_range(pbh, O):
+    g = O.make_graph(2, [(0, 1, 1)])
+    with pytest.raises(pbh.PreconditionError):
+        pbh.par_dijkstra(g, 2)
+
+
+@pytest.mark.parametrize("seed", range(1, 9))
+def test_random_graphs(pbh, O, seed):
+    check(pbh, O, O.gen_random(200, 1600, 50, seed))
+
+
+def test_high_diameter(pbh, O):
+    g = O.gen_high_diameter(1024, 10 * 1024, 100, 3)
+    r = check(pbh, O, g)
+    assert r.dist[1023] == 1023
+
+
+@pytest.mark.parametrize("d", [2, 7])
+def test_small_user_d(pbh, O, d):
+    check(pbh, O, O.gen_random(128, 1024, 30, 9), d=d)
+
+
+@pytest.mark.parametrize("outdeg", [1, 4, 16])
+def test_dag_mode(pbh, O, outdeg):
+    check(pbh, O, O.gen_dag(512, outdeg, 40, outdeg + 5), dag=True)
+
+
+def test_settled_monotone(pbh, O):
+    r = check(pbh, O, O.gen_random(300, 2400, 20, 17))
+    d = r.dist[r.settled_order]
+    assert np.all(d[1:] >= d[:-1])
+
+
+def test_tie_heavy(pbh, O):
+    # settled order == (dist, vid) order under many ties
+    for s in range(3):
+        check(pbh, O, O.gen_random(2000, 16000, 3, 100 + s))
+
+
+@pytest.mark.parametrize("v,epv", [(256, 4), (1024, 32), (4096, 256)])
+def test_acceptance_random_family(pbh, O, v, epv):
+    e = min(epv * v, v * (v - 1))
+    check(pbh, O, O.gen_random(v, e, 1000, v + epv))
+
+
+@pytest.mark.parametrize("v", [1024, 4096])
+def test_acceptance_high_diameter(pbh, O, v):
+    r = check(pbh, O, O.gen_high_diameter(v, 8 * v, 500, v))
+    assert r.dist[v - 1] == v - 1
+
+
+@pytest.mark.parametrize("outdeg", [8, 64])
+def test_acceptance_dag(pbh, O, outdeg):
+    check(pbh, O, O.gen_dag(4096, outdeg, 300, outdeg), dag=True)
+
+
+@pytest.mark.parametrize("v", [256, 512])
+def test_acceptance_complete(pbh, O, v):
+    check(pbh, O, O.gen_complete(v, 1000, v))
+
+
+def test_grid_and_band_small(pbh, O):
+    check(pbh, O, O.gen_grid(64, 64, 1))
+    check(pbh, O, O.gen_band(4096, 256, 2))
+
+
+def test_multi_source(pbh, O):
+    g = O.gen_band(4096, 64, 2)
+    sources = [i * 512 for i in range(8)]
+    dist, parent = pbh.par_dijkstra_multi(g, sources)
+    for i, s in enumerate(sources):
+        want = O.dijkstra(g, s)
+        assert np.array_equal(dist[i], want["dist"])
+        assert pbh.validate_parent_tree(g, s, dist[i], parent[i]) is None
+
+
+def test_golden_sssp_fixtures(pbh):
+    path = os.path.join(os.path.dirname(__file__), "golden", "sssp.npz")
+    z = np.load(path)
+    for name in [k[:-4] for k in z.files if k.endswith("_off")]:
+        g = pbh.CsrGraph(len(z[name + "_off"]) - 1, z[name + "_off"], z[name + "_tgt"],
+                         z[name + "_w"])
+        r = pbh.par_dijkstra(g, 0, dag_mode=bool(z[name + "_dag"]))
+        assert np.array_equal(r.dist, z[name + "_dist"]), name
+        assert np.array_equal(r.settled_order, z[name + "_settled"]), name
