@@ -46,6 +46,10 @@ const char* pbh_last_error(void);
 /* Library version string. */
 const char* pbh_version(void);
 
+/* Number of CUDA kernels this library has launched in the process so far
+ * (benchmark accounting of gpu_launches). */
+uint64_t pbh_launch_count(void);
+
 /* ---- heap lifecycle ---------------------------------------------------
  * Replaces pbh::Engine::Engine(EngineConfig{d, workers, debug_assertions})
  * (engine.hpp:49, engine.cpp:22-30) and BucketHeap(HeapConfig)

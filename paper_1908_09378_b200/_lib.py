@@ -30,6 +30,7 @@ class Csr(C.Structure):
 SIGNATURES = {
     "pbh_last_error": (C.c_char_p, []),
     "pbh_version": (C.c_char_p, []),
+    "pbh_launch_count": (C.c_uint64, []),
     "pbh_heap_create": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "pbh_heap_destroy": (C.c_int, [C.c_void_p]),
     "pbh_heap_update": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64]),

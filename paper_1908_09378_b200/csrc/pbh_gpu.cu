@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -12,13 +13,14 @@
 #include <vector>
 
 #include "../../include/pbh_gpu.h"
-#include "pbh_kernels.cuh"
+#include "pbh_fast.cuh"
 
 using namespace pbh_dev;
 
 namespace {
 
 thread_local std::string g_last_error;
+std::atomic<unsigned long long> g_launches{0};  // kernels launched by this library
 
 pbh_status set_err(pbh_status s, const std::string& msg) {
   g_last_error = msg;
@@ -34,6 +36,7 @@ pbh_status set_err(pbh_status s, const std::string& msg) {
   } while (0)
 
 constexpr int VT = 4;
+constexpr int kFastCap0 = 1024;  // B_0 capacity of the fast SSSP path (static smem)
 constexpr u32 kSmemLimit = 227 * 1024;
 
 u64 pow2_at_least(u64 x) {
@@ -109,6 +112,7 @@ cudaError_t launch_trace(const SmLayout& L, cudaStream_t st, pbh_heap_dev* g, pb
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
   if (err != cudaSuccess) return err;
   fn<<<1, NT, L.total, st>>>(g, tr, b, e, ov, op, ks, L, internal);
+  g_launches++;
   return cudaGetLastError();
 }
 
@@ -130,6 +134,7 @@ cudaError_t launch_sssp(const SmLayout& L, cudaStream_t st, u32 grid, pbh_heap_d
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
   if (err != cudaSuccess) return err;
   fn<<<grid, NT, L.total, st>>>(heaps, off, tgt, w, V, src, dist, settled, sst, dag, maxdeg, L);
+  g_launches++;
   return cudaGetLastError();
 }
 
@@ -142,6 +147,40 @@ cudaError_t launch_sssp_nt(int nt, const SmLayout& L, cudaStream_t st, u32 grid,
     case 256: return launch_sssp<256>(L, st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, dag, maxdeg);
     default: return launch_sssp<1024>(L, st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, dag, maxdeg);
   }
+}
+
+FastLayout make_fast_layout(u32 cap0) {
+  FastLayout L{};
+  u32 off = 0;
+  L.off_hs = off; off += a16(sizeof(HeapSmem<32, VT>));
+  for (int s = 0; s < 2; ++s) { L.off_bk[s] = off; off += a16((u64)cap0 * 4); }
+  for (int s = 0; s < 2; ++s) { L.off_bp[s] = off; off += a16((u64)cap0 * 8); }
+  for (int s = 0; s < 2; ++s) { L.off_bt[s] = off; off += a16(cap0); }
+  L.off_sk = off; off += a16(kFastS0 * 4);
+  L.off_sp = off; off += a16(kFastS0 * 8);
+  L.off_sv = off; off += a16(kFastS0);
+  L.off_tk = off; off += a16(kFastS0 * 4);
+  L.off_tp = off; off += a16(kFastS0 * 8);
+  L.off_pk = off; off += a16((u64)2 * kFastS0 * 4);
+  L.off_pp = off; off += a16((u64)2 * kFastS0 * 8);
+  L.off_cpos = off; off += a16(((u64)std::max<u32>(cap0, kFastS0) + 64) * 4);
+  L.off_ck = off; off += a16(kChunk * 4);
+  L.off_cp = off; off += a16(kChunk * 8);
+  L.off_co = off; off += a16(kChunk * 8);
+  L.off_cs = off; off += a16(kChunk * 4);
+  L.off_kf = off; off += a16(kChunk);
+  L.total = off;
+  return L;
+}
+
+cudaError_t launch_sssp_fast(const FastLayout& L, cudaStream_t st, u32 grid, pbh_heap_dev* heaps,
+                             const u64* off, const u32* tgt, const u32* w, u32 V, const u32* src,
+                             u64* dist, u32* settled, SsspState* sst, u32 dag, u32 maxdeg, u32 d) {
+  auto fn = k_sssp_fast<kFastCap0, VT>;
+  static const u32 xp = getenv("PBH_XP") ? (u32)atoi(getenv("PBH_XP")) : 0u;
+  fn<<<grid, 32, 0, st>>>(heaps, off, tgt, w, V, src, dist, settled, sst, dag, maxdeg, d, L, xp);
+  g_launches++;
+  return cudaGetLastError();
 }
 
 __global__ void k_finalize_parent(const pbh_idx_entry* idx, u32 V, u32* parent) {
@@ -324,6 +363,9 @@ struct pbh_heap {
 namespace {
 
 pbh_status ensure_staging(pbh_heap* h, u64 n_ops, u64 n_el, u64 n_out) {
+  n_ops = std::max<u64>(n_ops, 1);
+  n_el = std::max<u64>(n_el, 1);
+  n_out = std::max<u64>(n_out, 1);
   if (n_ops > h->st_ops) {
     cudaFree(h->d_kinds);
     cudaFree(h->d_off);
@@ -483,6 +525,7 @@ extern "C" {
 
 const char* pbh_last_error(void) { return g_last_error.c_str(); }
 const char* pbh_version(void) { return "pbh-b200 0.1 (sm_100a)"; }
+uint64_t pbh_launch_count(void) { return g_launches.load(); }
 
 pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int debug_checks,
                            pbh_heap** out) {
@@ -787,6 +830,8 @@ struct pbh_sssp_ctx {
   u32 cap0 = 0;
   u64 max_sources = 0;
   SmLayout layout{};
+  FastLayout flayout{};
+  bool fast = true;
   std::vector<DevHeap> heaps;
   pbh_heap_dev* d_heaps = nullptr;
   SsspState* d_sst = nullptr;
@@ -853,6 +898,7 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
   cudaMemsetAsync(d_md, 0, 8, c->stream);
   k_max_degree<<<std::max<u32>(1, std::min<u32>(1184, (c->V + 255) / 256)), 256, 0, c->stream>>>(
       c->d_off, c->V, d_md);
+  g_launches++;
   unsigned long long md = 0;
   cudaMemcpyAsync(&md, d_md, 8, cudaMemcpyDeviceToHost, c->stream);
   if (cudaStreamSynchronize(c->stream) != cudaSuccess)
@@ -862,6 +908,12 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
   c->d = std::min<u64>(c->d, std::max<u64>(1, md ? md : 1));  // batches never exceed a row
   c->nt = pick_nt(std::max<u64>(c->d, std::min<u64>(md, 1024)));
   c->cap0 = pick_cap0(c->d);
+  if (const char* e = getenv("PBH_SSSP_ENGINE")) c->fast = std::string(e) != "cta";
+  if (c->fast) {
+    c->cap0 = kFastCap0;
+    c->nt = 32;
+    c->flayout = make_fast_layout(c->cap0);
+  }
   const u32 bc = (u32)pow2_at_least(std::max<u64>(c->d, 2));
   c->layout = make_layout(c->nt, c->cap0, bc, (u32)c->d, true);
   if ((st = ctx_alloc(c, (void**)&c->d_heaps, max_sources * sizeof(pbh_heap_dev)))) return fail(st);
@@ -922,9 +974,15 @@ pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n
   std::vector<SsspState> hs(n_sources);
   for (int guard = 0; guard < 256; ++guard) {
     CK(cudaEventRecord(c->ev0, c->stream));
-    CK(launch_sssp_nt(c->nt, c->layout, c->stream, (u32)n_sources, c->d_heaps, c->d_off, c->d_tgt,
-                      c->d_w, c->V, c->d_src, c->d_dist, c->d_settled, c->d_sst, dag_mode ? 1 : 0,
-                      c->max_deg));
+    if (c->fast) {
+      CK(launch_sssp_fast(c->flayout, c->stream, (u32)n_sources, c->d_heaps, c->d_off, c->d_tgt,
+                          c->d_w, c->V, c->d_src, c->d_dist, c->d_settled, c->d_sst,
+                          dag_mode ? 1 : 0, c->max_deg, (u32)std::min<u64>(c->d, 0xffffffffu)));
+    } else {
+      CK(launch_sssp_nt(c->nt, c->layout, c->stream, (u32)n_sources, c->d_heaps, c->d_off,
+                        c->d_tgt, c->d_w, c->V, c->d_src, c->d_dist, c->d_settled, c->d_sst,
+                        dag_mode ? 1 : 0, c->max_deg));
+    }
     CK(cudaEventRecord(c->ev1, c->stream));
     CK(cudaMemcpyAsync(hs.data(), c->d_sst, n_sources * sizeof(SsspState), cudaMemcpyDeviceToHost,
                        c->stream));
@@ -952,11 +1010,20 @@ pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n
   for (u64 i = 0; i < n_sources; ++i) {
     k_finalize_parent<<<std::max<u32>(1, std::min<u32>(1184, (c->V + 255) / 256)), 256, 0,
                         c->stream>>>(c->heaps[i].hd.idx, c->V, c->d_parent + i * c->V);
+    g_launches++;
   }
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->stream));
   c->n_last = n_sources;
   if (device_ms) *device_ms = ms_total;
+  if (getenv("PBH_PHASES")) {
+    SsspState s0;
+    cudaMemcpy(&s0, c->d_sst, sizeof s0, cudaMemcpyDeviceToHost);
+    const double r = s0.rounds ? (double)s0.rounds : 1.0;
+    fprintf(stderr, "phases cyc/round: extract %.0f relax %.0f kill %.0f append %.0f tail %.0f | flush %.0f (n=%llu) smin %.0f | pf_hits %.3f\n",
+            s0.phase[0] / r, s0.phase[1] / r, s0.phase[2] / r, s0.phase[3] / r, s0.phase[4] / r,
+            s0.phase[5] / r, (unsigned long long)s0.pad2, s0.phase[6] / r, s0.phase[7] / r);
+  }
   return PBH_OK;
 }
 
@@ -975,9 +1042,13 @@ pbh_status pbh_sssp_ctx_fetch(pbh_sssp_ctx* c, uint64_t slot, uint64_t* dist, ui
   if (n_settled) *n_settled = s.n_settled;
   if (rounds) *rounds = s.rounds;
   if (ops) {
-    u64 o = 0;
-    CK(cudaMemcpy(&o, &c->heaps[slot].dev->ops, 8, cudaMemcpyDeviceToHost));
-    *ops = o;
+    if (c->fast) {
+      *ops = s.ops;
+    } else {
+      u64 o = 0;
+      CK(cudaMemcpy(&o, &c->heaps[slot].dev->ops, 8, cudaMemcpyDeviceToHost));
+      *ops = o;
+    }
   }
   return PBH_OK;
 }

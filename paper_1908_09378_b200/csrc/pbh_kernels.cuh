@@ -25,6 +25,9 @@ struct SsspState {
   u32 detail;
   u32 pad;
   u64 aux;
+  u64 ops;  // Metrics::ops of par_dijkstra (fast path)
+  u64 pad2;
+  u64 phase[8];  // clock64 cycles per phase (PBH_PHASES diagnostics)
 };
 
 // Internal op kinds (never accepted from user traces).

@@ -6,8 +6,8 @@ import re
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_symbols():
-    src = open(os.path.join(ROOT, "include", "pbh_gpu.h")).read()
+def declared_symbols(header="pbh_gpu.h"):
+    src = open(os.path.join(ROOT, "include", header)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(pbh_[a-z0-9_]+)\s*\(", src)))
 
@@ -22,8 +22,11 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_python_mirror_binds_every_symbol():
-    from paper_1908_09378_b200 import _lib
+    from paper_1908_09378_b200 import _lib, gen
     assert set(declared_symbols()) == set(_lib.SIGNATURES)
+    assert set(declared_symbols("pbh_gen.h")) == set(gen.GEN_SIGNATURES)
+    L = _lib.lib()
+    assert all(hasattr(L, s) for s in gen.GEN_SIGNATURES)
 
 
 def test_version_and_error_without_gpu():
