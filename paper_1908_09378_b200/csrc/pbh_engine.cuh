@@ -52,7 +52,7 @@ DEV bool admits(const pbh_level_state& s, u64 p, u32 k) {
 
 DEV bool entry_valid(const pbh_idx_entry* idx, u32 k, u64 p) {
   const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + k));
-  return (u32)e.y == PBH_ST_LIVE && e.x == p;
+  return PBH_ST((u32)e.y) == PBH_ST_LIVE && e.x == p;
 }
 
 // --------------------------------------------------------------------------

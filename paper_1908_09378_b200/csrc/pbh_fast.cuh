@@ -40,6 +40,7 @@ struct FastSmem {
   u32 cs[kChunk];
   u8 sv[kFastS0];
   u8 kf[kChunk];
+  u32 sh[2 * kFastS0];  // key -> S_0 slot + 1 (open addressing; 0 = empty)
   HeapSmem<32, VT> hs;
 };
 
@@ -67,9 +68,18 @@ struct FastSssp {
   using HC = HeapCta<32, VT>;
   HC& hc;
   const u32 lane;
+  pbh_idx_entry* idx;
   static constexpr u32 cap0 = CAP0;
 
-  DEV FastSssp(HC& h, u32 ln) : hc(h), lane(ln) {}
+  DEV FastSssp(HC& h, u32 ln, pbh_idx_entry* ix) : hc(h), lane(ln), idx(ix) {}
+
+  DEV void set_loc(u32 k, u32 loc) { idx[k].state = PBH_ST_LIVE | (loc << 2); }
+  // Relabel every B_0 entry with its slot (after B_0 was rebuilt elsewhere).
+  DEV void relabel_b0() {
+    for (u32 i = bh + lane; i < be; i += 32)
+      if (!bt(bsel)[i]) set_loc(bk(bsel)[i], PBH_LOC_B | i);
+    __syncwarp();
+  }
   // replicated scalar state
   u32 bsel, bh, be;    // B_0 = bk[bsel][bh, be)
   u32 b_live;
@@ -97,6 +107,8 @@ struct FastSssp {
   DEV u32* pk() const { return Sm().pk; }
   DEV u64* pp() const { return Sm().pp; }
   DEV u32* cpos() const { return Sm().cpos; }
+  DEV u32* sh() const { return Sm().sh; }
+  DEV static u32 hslot(u32 k) { return (k * 2654435761u) >> (32 - 7); }  // 128 buckets
 
   DEV bool adm0(u64 p, u32 k) const { return spl_inf || p < spl_p || (p == spl_p && k <= spl_k); }
 
@@ -106,21 +118,22 @@ struct FastSssp {
     return __popc(m & ((1u << (threadIdx.x & 31)) - 1));
   }
 
-  // warp argmin of (p, k, tag) over lanes with `has`
+  // warp argmin of (p, k, tag) over lanes with `has`: three redux.sync
+  // minimum reductions (high word, low word, key) instead of a shuffle tree.
   DEV static void wmin(bool& has, u64& p, u32& k, u32& tag) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const u64 op = __shfl_xor_sync(0xffffffffu, p, o);
-      const u32 ok = __shfl_xor_sync(0xffffffffu, k, o);
-      const u32 ot = __shfl_xor_sync(0xffffffffu, tag, o);
-      const bool oh = __shfl_xor_sync(0xffffffffu, has, o);
-      if (oh && (!has || less_pk(op, ok, p, k))) {
-        p = op;
-        k = ok;
-        tag = ot;
-        has = true;
-      }
-    }
+    const u32 hi = has ? (u32)(p >> 32) : 0xffffffffu;
+    const u32 mhi = __reduce_min_sync(0xffffffffu, hi);
+    const bool c1 = has && hi == mhi;
+    const u32 lo = c1 ? (u32)p : 0xffffffffu;
+    const u32 mlo = __reduce_min_sync(0xffffffffu, lo);
+    const bool c2 = c1 && (u32)p == mlo;
+    const u32 mk = __reduce_min_sync(0xffffffffu, c2 ? k : 0xffffffffu);
+    const u32 win = __ballot_sync(0xffffffffu, c2 && k == mk);
+    const bool any = __any_sync(0xffffffffu, has);
+    tag = __shfl_sync(0xffffffffu, tag, win ? __ffs(win) - 1 : 0);
+    p = ((u64)mhi << 32) | mlo;
+    k = mk;
+    has = any;
   }
 
   // ---------------------------------------------------------- state sync
@@ -284,9 +297,11 @@ struct FastSssp {
       if (pos < cap0) {
         OK[pos] = k;
         OP[pos] = p;
+        set_loc(k, PBH_LOC_B | pos);
       } else {
         PK[pos - cap0] = k;
         PP[pos - cap0] = p;
+        set_loc(k, PBH_LOC_DEEP);
       }
     };
     for (u32 b = bh; b < be; b += 32) {
@@ -311,6 +326,7 @@ struct FastSssp {
     for (u32 j = adm + lane; j < n_s; j += 32) {
       PK[n_push + j - adm] = SK[j];
       PP[n_push + j - adm] = SP[j];
+      set_loc(SK[j], PBH_LOC_DEEP);
     }
     n_push += n_s - adm;
     u8* NT = bt(nb);
@@ -345,6 +361,7 @@ struct FastSssp {
     else
       hc.refill(0);
     from_cold();
+    relabel_b0();
   }
 
   DEV void skip_b() {
@@ -389,40 +406,42 @@ struct FastSssp {
 
   // --------------------------------------------------------- kill/insert
   // Eagerly remove the old copies of the decreased keys among the n
-  // candidates (ck/co/cs in smem) from S_0 (parallel slot scan) or B_0
-  // (binary search). Copies deeper are dropped lazily by the HBM filters.
-  DEV void kill(const u32* ck, const u64* co, const u32* cs, u8* kf, u32 n) {
-    for (u32 j = lane; j < n; j += 32) kf[j] = 0;
-    __syncwarp();
+  // candidates (ck/co/cs in smem). The old index entry read at relax time
+  // carries the copy's level-0 location (S_0 slot or B_0 slot), so a kill is
+  // one verified O(1) tombstone; copies in HBM levels are dropped lazily by
+  // the merge filters. A binary-search fallback guards a stale location.
+  DEV void kill(const u32* ck, const u64* co, const u32* cs, u32 n) {
     bool smin_hit = false;
-    u32 ks = 0;
-    if (s_live) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const u32 i = lane + 32 * h;
-        if (i < s0n && sv()[i]) {
-          const u32 k = sk()[i];
-          const u64 p = sp()[i];
-          for (u32 j = 0; j < n; ++j) {
-            if (ck[j] == k && co[j] == p && cs[j] == PBH_ST_LIVE) {
-              sv()[i] = 0;
-              kf[j] = 1;
-              ++ks;
-              smin_hit |= i == smin_slot;
-              break;
-            }
+    u32 ks = 0, kb = 0;
+    for (u32 j = lane; j < n; j += 32) {
+      const u32 sw = cs[j];
+      if (PBH_ST(sw) != PBH_ST_LIVE) continue;
+      const u32 loc = sw >> 2;
+      if (loc == PBH_LOC_DEEP) continue;
+      const u32 k = ck[j];
+      const u64 po = co[j];
+      // 1) the recorded S_0 slot (or a scan when the slot is stale)
+      bool found = false;
+      if (!(loc & PBH_LOC_B) && s0n) {
+        u32 i = loc;
+        if (!(i < s0n && sk()[i] == k && sp()[i] == po))
+          for (i = 0; i < s0n && !(sk()[i] == k && sp()[i] == po && sv()[i]); ++i) {
           }
+        if (i < s0n && sv()[i]) {
+          sv()[i] = 0;
+          ++ks;
+          smin_hit |= i == smin_slot;
+          found = true;
         }
       }
-    }
-    __syncwarp();
-    u32 kb = 0;
-    for (u32 j = lane; j < n; j += 32) {
-      if (cs[j] == PBH_ST_LIVE && !kf[j] && adm0(co[j], ck[j])) {
+      // 2) the recorded B_0 slot (or a binary search when it is stale)
+      if (!found && adm0(po, k)) {
         const u32* K = bk(bsel);
         const u64* P = bp(bsel);
-        const u32 i = lbound(K, P, bh, be, co[j], ck[j]);
-        if (i < be && K[i] == ck[j] && P[i] == co[j] && !bt(bsel)[i]) {
+        u32 i = loc & ~PBH_LOC_B;
+        if (!((loc & PBH_LOC_B) && i >= bh && i < be && K[i] == k && P[i] == po))
+          i = lbound(K, P, bh, be, po, k);
+        if (i < be && K[i] == k && P[i] == po && !bt(bsel)[i]) {
           bt(bsel)[i] = 1;
           ++kb;
         }
@@ -436,7 +455,7 @@ struct FastSssp {
 
   // Append the n candidates (ck/cp) to S_0; (gm_p, gm_k, gm_j) is their
   // minimum and its list index.
-  DEV void append(const u32* ck, const u64* cp, u32 n, u64 gm_p, u32 gm_k, u32 gm_j) {
+  DEV void append(const u32* ck, const u64* cp, u32 n, u64 gm_p, u32 gm_k, u32 gm_j, u32 par) {
     u32 done = 0;
     while (done < n) {
       if (s0n >= (u32)kFastS0) {
@@ -445,9 +464,16 @@ struct FastSssp {
       }
       const u32 m = min(n - done, (u32)kFastS0 - s0n);
       for (u32 j = lane; j < m; j += 32) {
-        sk()[s0n + j] = ck[done + j];
-        sp()[s0n + j] = cp[done + j];
+        const u32 k = ck[done + j];
+        const u64 pk_ = cp[done + j];
+        sk()[s0n + j] = k;
+        sp()[s0n + j] = pk_;
         sv()[s0n + j] = 1;
+        pbh_idx_entry e;
+        e.prio = pk_;
+        e.state = PBH_ST_LIVE | ((s0n + j) << 2);
+        e.parent = par;
+        reinterpret_cast<ulonglong2*>(idx)[k] = *reinterpret_cast<const ulonglong2*>(&e);
       }
       __syncwarp();
       if (done == 0 && m == n) {
@@ -489,12 +515,13 @@ __global__ void __launch_bounds__(32, 1)
   hc.pp = g->g_pp;
   hc.rm = g->g_rm;
   hc.bo = nullptr;
-  FastSssp<CAP0, VT> F(hc, threadIdx.x);
+  FastSssp<CAP0, VT> F(hc, threadIdx.x, g->idx);
   F.xp_ = xp;
   F.s0n = 0;
   F.s_live = 0;
   F.pushes = sm.ops;  // persisted push counter (fast path reuses the ops slot)
   F.from_cold();
+  F.relabel_b0();  // B_0 was reloaded at offset 0
   pbh_idx_entry* idx = g->idx;
   u64* my_dist = dist + (u64)blockIdx.x * V;
   u32* my_settled = settled + (u64)blockIdx.x * V;
@@ -510,26 +537,18 @@ __global__ void __launch_bounds__(32, 1)
   if (!my->started) {
     const u32 s = sources[blockIdx.x];
     if (lane == 0) {
-      pbh_idx_entry e;
-      e.prio = 0;
-      e.state = PBH_ST_LIVE;
-      e.parent = s;
-      idx[s] = e;
       ck[0] = s;
       cpv[0] = 0;
     }
     __syncwarp();
-    F.append(ck, cpv, 1, 0, s, 0);
+    F.append(ck, cpv, 1, 0, s, 0, s);
     F.live = 1;
     ops = 1;  // eng.update({s, 0}) (sssp.cpp:36)
   }
 
   bool need_grow = false, overflow = false;
-  // exact next-vertex prefetch: row bounds + first chunk of targets/weights
-  bool pf = false;
-  u32 pf_v = 0;
-  u64 pf_rb = 0, pf_re = 0;
-  u32 pu[8], pw[8];
+  const u32 Lnl = sm.n_levels;
+  const u64 cap_last = Lnl == 1 ? (u64)CAP0 : sm.lv[Lnl - 1].cap_b;
   const bool tm = (xp & 16) != 0;
   u64 ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tA = clock64(), tB;
@@ -539,15 +558,17 @@ __global__ void __launch_bounds__(32, 1)
     ph[i] += (u64)(tB - tA);    \
     tA = tB;                    \
   }
+  // Exact next-vertex prefetch: after the candidates of round r are known,
+  // the next extraction is min(live heads, new entries); its offsets load
+  // under the kill phase and its first row chunk under append + extract.
+  bool pf = false;
+  u32 pf_v = 0;
+  u64 pf_rb = 0, pf_re = 0;
+  u32 pu[8], pw[8];
   while (!hc.failed() && F.live > 0) {
-    {  // room check: the deepest allocated bucket must absorb everything
-      const u64 content = (u64)(F.be - F.bh) + F.s0n + F.deep_n;
-      const u32 Ln = sm.n_levels;
-      const u64 cap_last = Ln == 1 ? F.cap0 : sm.lv[Ln - 1].cap_b;
-      if (content + max_deg + kFastS0 > cap_last) {
-        need_grow = true;
-        break;
-      }
+    if ((u64)(F.be - F.bh) + F.s0n + F.deep_n + max_deg + kFastS0 > cap_last) {
+      need_grow = true;
+      break;
     }
     u32 v;
     u64 p;
@@ -564,7 +585,6 @@ __global__ void __launch_bounds__(32, 1)
     ++rounds;
     ++ops;
     PH(0);
-    // relax the CSR row of v (sssp.cpp:49-57)
     const bool hit = pf && pf_v == v;
     if (tm && hit) ph[7] += 1;
     u64 rb, re;
@@ -606,7 +626,7 @@ __global__ void __launch_bounds__(32, 1)
       for (int t = 0; t < 8; ++t) {
         const u64 j = base + lane + 32 * t;
         cand[t] = 0;
-        if (j < re && (dag_mode || (u32)ee[t].y != PBH_ST_DEAD)) {
+        if (j < re && (dag_mode || PBH_ST((u32)ee[t].y) != PBH_ST_DEAD)) {
           cand[t] = p + ww[t];
           overflow |= cand[t] < p;
           if (cand[t] < ee[t].x) mask |= 1u << t;
@@ -627,12 +647,7 @@ __global__ void __launch_bounds__(32, 1)
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         if (mask & (1u << t)) {
-          pbh_idx_entry e;
-          e.prio = cand[t];
-          e.state = PBH_ST_LIVE;
-          e.parent = v;
-          reinterpret_cast<ulonglong2*>(idx)[uu[t]] = *reinterpret_cast<const ulonglong2*>(&e);
-          nfresh += (u32)ee[t].y != PBH_ST_LIVE;
+          nfresh += PBH_ST((u32)ee[t].y) != PBH_ST_LIVE;
           ck[pos] = uu[t];
           cpv[pos] = cand[t];
           cov[pos] = ee[t].x;
@@ -649,51 +664,38 @@ __global__ void __launch_bounds__(32, 1)
       __syncwarp();
       F.live += __reduce_add_sync(0xffffffffu, nfresh);
       n_imp += tot;
-      if (tot == 0) {
-        if (last_chunk) {
-          // next extraction = current minimum (nothing new this chunk)
-          F.skip_b();
-          const bool hb = F.bh < F.be;
-          if (hb || F.s_live) {
-            const bool tb = hb && (!F.s_live || less_pk(F.bp(F.bsel)[F.bh], F.bk(F.bsel)[F.bh],
-                                                         F.smin_p, F.smin_k));
-            pf_v = tb ? F.bk(F.bsel)[F.bh] : F.smin_k;
-            pf = true;
-            pf_rb = off[pf_v];
-            pf_re = off[pf_v + 1];
-          }
-        }
-        continue;
-      }
-      FastSssp<CAP0, VT>::wmin(bany, bp_, bk_, bj_);
+      if (tot) FastSssp<CAP0, VT>::wmin(bany, bp_, bk_, bj_);
       if (last_chunk) {
-        // exact next extraction = min(live heads, new entries); a killed
-        // head's replacement is among the new entries and smaller
         F.skip_b();
         const bool hb = F.bh < F.be;
+        bool nh = bany;
         u32 nv = bk_;
         u64 np_ = bp_;
-        if (hb && less_pk(F.bp(F.bsel)[F.bh], F.bk(F.bsel)[F.bh], np_, nv)) {
+        if (hb && (!nh || less_pk(F.bp(F.bsel)[F.bh], F.bk(F.bsel)[F.bh], np_, nv))) {
           nv = F.bk(F.bsel)[F.bh];
           np_ = F.bp(F.bsel)[F.bh];
+          nh = true;
         }
-        if (F.s_live && less_pk(F.smin_p, F.smin_k, np_, nv)) nv = F.smin_k;
-        pf = true;
-        pf_v = nv;
-        pf_rb = off[pf_v];
-        pf_re = off[pf_v + 1];
+        if (F.s_live && (!nh || less_pk(F.smin_p, F.smin_k, np_, nv))) {
+          nv = F.smin_k;
+          nh = true;
+        }
+        if (nh && !(xp & 8)) {
+          pf = true;
+          pf_v = nv;
+          pf_rb = off[pf_v];
+          pf_re = off[pf_v + 1];
+        }
       }
       PH(1);
-      if (!(xp & 1)) F.kill(ck, cov, csv, kf, tot);
+      if (tot && !(xp & 1)) F.kill(ck, cov, csv, tot);
       PH(2);
-      if (!(xp & 2)) F.append(ck, cpv, tot, bp_, bk_, bj_);
+      if (tot && !(xp & 2)) F.append(ck, cpv, tot, bp_, bk_, bj_, v);
       PH(3);
       if (hc.failed()) break;
     }
-    PH(1);
-    if (xp & 8) pf = false;
+    if (hc.failed()) break;
     if (pf) {
-      // start loading the next vertex's first chunk while the loop turns
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const u64 j = pf_rb + lane + 32 * t;

@@ -186,7 +186,7 @@ cudaError_t launch_sssp_fast(const FastLayout& L, cudaStream_t st, u32 grid, pbh
 __global__ void k_finalize_parent(const pbh_idx_entry* idx, u32 V, u32* parent) {
   for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < V; v += (u64)gridDim.x * blockDim.x) {
     const pbh_idx_entry e = idx[v];
-    parent[v] = e.state == PBH_ST_DEAD ? e.parent : 0xffffffffu;
+    parent[v] = PBH_ST(e.state) == PBH_ST_DEAD ? e.parent : 0xffffffffu;
   }
 }
 
@@ -731,7 +731,7 @@ pbh_status pbh_heap_check_invariants(pbh_heap* h, uint64_t* n_violations) {
       prev_k = bk[t.b_size - 1];
     }
     auto valid = [&](u32 k, u64 p) {
-      return k < hd.universe && idx[k].state == PBH_ST_LIVE && idx[k].prio == p;
+      return k < hd.universe && PBH_ST(idx[k].state) == PBH_ST_LIVE && idx[k].prio == p;
     };
     for (u32 j = 0; j < t.b_size; ++j) {
       const bool ok = valid(bk[j], bp[j]);
@@ -741,7 +741,7 @@ pbh_status pbh_heap_check_invariants(pbh_heap* h, uint64_t* n_violations) {
     for (u32 j = 0; j < t.s_size; ++j) valid_entries += valid(sk[j], sp[j]);
   }
   u64 live_idx = 0;
-  for (const auto& e : idx) live_idx += e.state == PBH_ST_LIVE;
+  for (const auto& e : idx) live_idx += PBH_ST(e.state) == PBH_ST_LIVE;
   if ((i64)live_idx != hd.live)
     complain("live_size " + std::to_string(hd.live) + " != live index entries " +
              std::to_string(live_idx));

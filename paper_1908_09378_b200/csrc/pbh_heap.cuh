@@ -482,8 +482,8 @@ struct HeapCta {
         continue;
       }
       const pbh_idx_entry e = idx[k];
-      if (e.state == PBH_ST_DEAD) bad_dead = true;
-      if (s.debug && e.state == PBH_ST_LIVE && prios[j] > e.prio) bad_inc = true;
+      if (PBH_ST(e.state) == PBH_ST_DEAD) bad_dead = true;
+      if (s.debug && PBH_ST(e.state) == PBH_ST_LIVE && prios[j] > e.prio) bad_inc = true;
     }
     if (Bk::any(bad_sort, scr())) return fail(PBH_ERR_UNSORTED);
     if (Bk::any(bad_key, scr())) return fail(PBH_ERR_KEY_RANGE);
@@ -501,7 +501,7 @@ struct HeapCta {
         k = vals[j];
         p = prios[j];
         const pbh_idx_entry e = idx[k];
-        if (e.state != PBH_ST_LIVE) {
+        if (PBH_ST(e.state) != PBH_ST_LIVE) {
           ins = true;
           fresh++;
           idx[k].prio = p;
@@ -581,13 +581,13 @@ struct HeapCta {
     if (k >= g->universe) return;
     const pbh_idx_entry e = idx[k];
     Bk::sync();
-    if (e.state == PBH_ST_LIVE && admits(s.st[0], e.prio, k)) {
+    if (PBH_ST(e.state) == PBH_ST_LIVE && admits(s.st[0], e.prio, k)) {
       if (t0()) rm[b0_find(e.prio, k)] = 1;
       Bk::sync();
       insert_staged(0, true);
     }
     if (t0()) {
-      if (e.state == PBH_ST_LIVE) s.live -= 1;
+      if (PBH_ST(e.state) == PBH_ST_LIVE) s.live -= 1;
       idx[k].state = PBH_ST_DEAD;
     }
     Bk::sync();
@@ -608,7 +608,7 @@ struct HeapCta {
       e.state = PBH_ST_LIVE;
       e.parent = v;
       idx[k] = e;
-      if (st != PBH_ST_LIVE) {
+      if (PBH_ST(st) != PBH_ST_LIVE) {
         fresh++;
       } else if (admits(s.st[0], old, k)) {
         rm[b0_find(old, k)] = 1;

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(NT) k_sssp(pbh_heap_dev* heaps, const u64* __r
         const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + u));
         oldp = e.x;
         olds = (u32)e.y;
-        if (dag_mode || olds != PBH_ST_DEAD) {
+        if (dag_mode || PBH_ST(olds) != PBH_ST_DEAD) {
           cand = p + w;
           if (cand < p) overflow = true;
           imp = cand < oldp;

@@ -13,6 +13,12 @@
 #define PBH_ST_ABSENT 0xFFFFFFFFu
 #define PBH_ST_LIVE 1u
 #define PBH_ST_DEAD 2u
+// The low two bits of `state` hold the state (absent reads as 3); the fast
+// SSSP path keeps the key's level-0 location in the upper 30 bits:
+// loc = slot (S_0), PBH_LOC_B | slot (B_0), PBH_LOC_DEEP (an HBM level).
+#define PBH_ST(x) ((x) & 3u)
+#define PBH_LOC_B 0x20000000u
+#define PBH_LOC_DEEP 0x3FFFFFFFu
 
 typedef struct __attribute__((aligned(16))) {
   uint64_t prio;
