@@ -199,9 +199,11 @@ class Engine {
     double wall = 0;
     vals.push_back(0);
     prios.push_back(0);
-    detail::check(pbh_heap_run_trace(h_, trace.size(), kinds.data(), off.data(), vals.data(),
-                                     prios.data(), ov.data(), op.data(), &n_out, &failed, &wall),
-                  failed);
+    // sequence the call before reading `failed` (argument evaluation order is unspecified)
+    const pbh_status st = pbh_heap_run_trace(h_, trace.size(), kinds.data(), off.data(),
+                                             vals.data(), prios.data(), ov.data(), op.data(),
+                                             &n_out, &failed, &wall);
+    detail::check(st, failed);
     RunResult r;
     r.extracted.reserve(n_out);
     for (std::uint64_t i = 0; i < n_out; ++i) r.extracted.push_back(Element::live(ov[i], op[i]));
