@@ -1,0 +1,638 @@
+// Banked level 0 for par_dijkstra (sssp.cpp:21-69): the default SSSP engine.
+//
+// One CTA of NW warps (B = 32*NW threads) owns one source's bucket heap.
+// Level 0 (everything <= splitter_0, bucket_heap.hpp:37-41) is an UNSORTED
+// slot array in shared memory, banked by thread: slot s = i*B + t belongs to
+// thread t, which keeps its bank's occupancy mask and minimum in registers.
+//   extract_min   = a CTA argmin of the B bank minima (three redux.sync per
+//                   warp, one barrier), then the owner rescans its bank;
+//   insert        = the relaxing thread takes a free slot of its own bank;
+//   decrease-key  = in place: the position index records the slot, the
+//                   relaxing thread overwrites the priority and flags the
+//                   owner, which rescans its bank in the next pass.
+// Each slot carries its vertex's CSR row (begin, degree), captured from the
+// offsets gathered with the index entry at relax time, so the extracted
+// vertex's row needs no dependent offsets load.
+//
+// A round relaxes the extracted vertex's row in passes of 256 edges (256/B
+// per thread, thread t taking the edges j with (j - round) mod B == t so the
+// new slots spread over the banks). Every pass ends with ONE barrier that
+// exchanges each warp's best offer (its bank minima and its applied admitted
+// candidates) and its counters. After the last pass that argmin IS the next
+// extraction: a decreased slot's stale bank minimum is larger than the
+// candidate that replaced it, and that candidate is offered by its writer.
+// So the next row's first pass is loaded before the round's bookkeeping and
+// the owners' rescans, which run under its latency.
+//
+// Deeper levels are the CTA engine of pbh_heap.cuh in HBM (cold path):
+//   * candidates beyond splitter_0 collect in a push buffer, sorted and
+//     merged into S_1 (push_down) in batches;
+//   * when a bank runs out of room for a pass, level 0 is sorted, the largest
+//     half is pushed into S_1 and the splitter lowered (the capacity cut of
+//     bucket_heap.cpp:205-219); the kept half is redistributed round-robin;
+//   * when level 0 empties, fill0() refills it with the smallest cap0
+//     entries of the deeper levels (bucket_heap.cpp:228-271);
+//   * resolve(i) runs after every 4^i-th push (scheduler.cpp:11-20).
+// Stale copies below level 0 are dropped by the index filter of every merge.
+#pragma once
+
+#include "pbh_kernels.cuh"
+
+namespace pbh_dev {
+
+constexpr int kBankQ = 512;     // push-buffer capacity (entries beyond the splitter)
+constexpr int kBankPass = 256;  // edges relaxed per pass
+
+// The part of the shared-memory image that survives a NEED_GROW relaunch.
+template <int B, int KI>
+struct BankL0 {
+  static constexpr int C0 = B * KI;
+  u64 lp[C0];    // slot priority
+  u64 lrb[C0];   // slot vertex's CSR row begin
+  u32 lk[C0];    // slot key (vertex)
+  u32 ldeg[C0];  // slot vertex's out-degree
+  u64 qp[kBankQ];
+  u32 qk[kBankQ];
+  u32 occ[B];    // per-thread occupancy masks (bit i = slot i*B + t)
+  u64 spl_p;
+  u32 spl_k, spl_inf, qn, pad;
+};
+
+// One warp's offer and counters for the per-pass exchange.
+struct BankOffer {
+  u64 p, rb;
+  u32 k, slot, deg, has;
+  u32 fresh, nimp, nq, flags;  // flags: 1 evict due, 2 bad slot, 4 overflow
+};
+
+template <int NW, int KI, int VT>
+struct BankSmem {
+  static constexpr int B = 32 * NW;
+  static constexpr int C0 = B * KI;
+  BankL0<B, KI> l0;
+  // cold-engine B_0 ping-pong (capacity C0/2 each); as one C0-entry array
+  // it is also the sort scratch of evict()
+  u32 bk[2][C0 / 2];
+  u64 bp[2][C0 / 2];
+  BankOffer ex[2][NW];  // per-pass exchange (parity double-buffered)
+  u8 dirty[2][B];       // decreased-bank flags (parity double-buffered)
+  HeapSmem<B, VT> hs;
+};
+
+template <int NW, int KI, int VT>
+DEV BankSmem<NW, KI, VT>& bank_smem() {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  return *reinterpret_cast<BankSmem<NW, KI, VT>*>(dyn);
+}
+
+// warp argmin of (p, k) over lanes with `has`; returns the winning lane.
+DEV u32 warp_argmin(bool& has, u64& p, u32& k) {
+  const u32 hi = has ? (u32)(p >> 32) : 0xffffffffu;
+  const u32 mhi = __reduce_min_sync(0xffffffffu, hi);
+  const bool c1 = has && hi == mhi;
+  const u32 lo = c1 ? (u32)p : 0xffffffffu;
+  const u32 mlo = __reduce_min_sync(0xffffffffu, lo);
+  const bool c2 = c1 && (u32)p == mlo;
+  const u32 mk = __reduce_min_sync(0xffffffffu, c2 ? k : 0xffffffffu);
+  const u32 win = __ballot_sync(0xffffffffu, c2 && k == mk);
+  has = win != 0;
+  p = ((u64)mhi << 32) | mlo;
+  k = mk;
+  return win ? __ffs(win) - 1 : 0;
+}
+
+template <int NW, int KI, int VT>
+struct BankHeap {
+  static constexpr int B = 32 * NW;
+  static constexpr int C0 = B * KI;
+  static constexpr u32 PE = kBankPass / B;  // edges per thread per pass
+  static_assert(KI <= 32, "occupancy mask is 32 bits");
+  static_assert(KI >= (int)PE, "a bank must hold one pass of inserts");
+  using HC = HeapCta<B, VT>;
+  using Bk = Blk<B>;
+  using SM = BankSmem<NW, KI, VT>;
+  HC& hc;
+  SM& S;
+  BankL0<B, KI>& L;
+  pbh_idx_entry* idx;
+  const u64* off;
+  const u32 tid;
+  // per-thread
+  u32 occm;
+  bool lhas;
+  u64 lmin_p;
+  u32 lmin_k, lmin_s;
+  // replicated
+  i64 live;
+  u64 pushes;
+  u64 deep_n;
+  u32 n_l0;
+  u32 qn;  // push-buffer fill (mirrors L.qn at pass boundaries)
+
+  DEV BankHeap(HC& h, SM& s, pbh_idx_entry* ix, const u64* of)
+      : hc(h), S(s), L(s.l0), idx(ix), off(of), tid(threadIdx.x) {}
+
+  DEV bool adm(u64 p, u32 k) const {
+    return L.spl_inf || p < L.spl_p || (p == L.spl_p && k <= L.spl_k);
+  }
+
+  // Recompute this thread's bank minimum.
+  DEV void rescan() {
+    lhas = false;
+    u32 m = occm;
+    while (m) {
+      const u32 i = __ffs(m) - 1;
+      m &= m - 1;
+      const u32 s = i * B + tid;
+      const u64 p = L.lp[s];
+      const u32 k = L.lk[s];
+      if (!lhas || less_pk(p, k, lmin_p, lmin_k)) {
+        lhas = true;
+        lmin_p = p;
+        lmin_k = k;
+        lmin_s = s;
+      }
+    }
+  }
+
+  // ------------------------------------------------------------ cold glue
+  DEV void to_cold() {
+    Bk::sync();
+    if (tid == 0) {
+      pbh_level_state& t = hc.s.st[0];
+      t.b_head = 0;
+      t.b_size = 0;
+      t.spl_p = L.spl_p;
+      t.spl_k = L.spl_k;
+      t.spl_inf = L.spl_inf;
+      hc.s.live = live;
+    }
+    Bk::sync();
+  }
+  DEV void after_cold() { deep_n = hc.content_from(1); }
+
+  // Merge the sorted run (K, P)[0, n) into S_1 and run the 4-to-1 schedule.
+  NOINL void push_run(const u32* K, const u64* P, u32 n) {
+    if (n == 0) return;
+    to_cold();
+    hc.template push_down<true>(0, Run{K, P, n});
+    ++pushes;
+    for (u32 i = 1; i < hc.s.n_levels && i < 31 && !hc.failed(); ++i) {
+      if (pushes & ((1ull << (2 * i)) - 1)) break;  // resolve(i) every 4^i pushes
+      hc.resolve(i);
+    }
+    after_cold();
+  }
+
+  NOINL void flush_q() {
+    Bk::sync();
+    const u32 n = qn;
+    if (n == 0) return;
+    bitonic_sort<B>(L.qk, L.qp, n);
+    push_run(L.qk, L.qp, n);
+    if (tid == 0) L.qn = 0;
+    qn = 0;
+    Bk::sync();
+  }
+
+  // Rebuild level 0 from the sorted run (K, P)[0, n), n <= C0: entry j goes
+  // to slot j (round-robin over the banks), rows reloaded from the offsets.
+  NOINL void rebuild(const u32* K, const u64* P, u32 n) {
+    Bk::sync();
+    occm = 0;
+    for (u32 j = tid; j < n; j += B) {
+      const u32 k = K[j];
+      const u64 rb = __ldg(off + k), re = __ldg(off + k + 1);
+      L.lk[j] = k;
+      L.lp[j] = P[j];
+      L.lrb[j] = rb;
+      L.ldeg[j] = (u32)(re - rb);
+      idx[k].state = PBH_ST_LIVE | (j << 2);
+      occm |= 1u << (j / B);
+    }
+    lhas = tid < n;
+    if (lhas) {
+      lmin_p = P[tid];
+      lmin_k = K[tid];
+      lmin_s = tid;
+    }
+    n_l0 = n;
+    Bk::sync();
+  }
+
+  // A bank lacks room for one pass: sort level 0, keep the smallest C0/2
+  // (splitter lowered to the last kept one), push the rest down.
+  NOINL void evict() {
+    u32* SK = &S.bk[0][0];
+    u64* SP = &S.bp[0][0];
+    Bk::sync();
+    u32 n = 0;
+    for (u32 i = 0; i < (u32)KI; ++i) {
+      const bool f = (occm >> i) & 1u;
+      u32 tot;
+      const u32 pos = n + Bk::scan_excl(f ? 1u : 0u, tot, hc.scr());
+      if (f) {
+        const u32 s = i * B + tid;
+        SK[pos] = L.lk[s];
+        SP[pos] = L.lp[s];
+      }
+      n += tot;
+    }
+    Bk::sync();
+    bitonic_sort<B>(SK, SP, n);
+    const u32 keep = n < (u32)C0 / 2 ? n : (u32)C0 / 2;
+    if (n > keep) {
+      if (tid == 0) {
+        L.spl_inf = 0;
+        L.spl_p = SP[keep - 1];
+        L.spl_k = SK[keep - 1];
+      }
+      for (u32 j = keep + tid; j < n; j += B) idx[SK[j]].state = PBH_ST_LIVE | (PBH_LOC_DEEP << 2);
+    }
+    rebuild(SK, SP, keep);
+    push_run(SK + keep, SP + keep, n - keep);
+  }
+
+  // Level 0 is empty: refill it from the deeper levels (cold fill0).
+  NOINL void refill() {
+    flush_q();
+    if (hc.failed()) return;
+    to_cold();
+    hc.fill0();
+    if (hc.failed()) return;
+    const Run b = hc.bucket(0);
+    if (tid == 0) {
+      const pbh_level_state& t = hc.s.st[0];
+      L.spl_inf = t.spl_inf;
+      L.spl_p = t.spl_p;
+      L.spl_k = t.spl_k;
+    }
+    rebuild(b.k, b.p, b.n);
+    if (tid == 0) {
+      hc.s.st[0].b_head = 0;
+      hc.s.st[0].b_size = 0;
+    }
+    Bk::sync();
+    after_cold();
+  }
+
+  // Per-pass exchange: CTA argmin of the offers (has, p, k) with their slot
+  // and row, and sums of the counters. One barrier.
+  DEV BankOffer exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u32 deg, u32 fresh,
+                         u32 nimp, u32 nq, u32 flags) {
+    const u32 lane = tid & 31, w = tid >> 5;
+    bool h = has;
+    u64 wp = p;
+    u32 wk = k;
+    const u32 wl = warp_argmin(h, wp, wk);
+    const u32 sf = __reduce_add_sync(0xffffffffu, fresh);
+    const u32 sn = __reduce_add_sync(0xffffffffu, nimp);
+    const u32 sq = __reduce_add_sync(0xffffffffu, nq);
+    const u32 fl = __reduce_or_sync(0xffffffffu, flags);
+    BankOffer& o = S.ex[par][w];
+    if (lane == wl) {
+      o.p = wp;
+      o.k = wk;
+      o.has = h;
+      o.slot = slot;
+      o.rb = rb;
+      o.deg = deg;
+      o.fresh = sf;
+      o.nimp = sn;
+      o.nq = sq;
+      o.flags = fl;
+    }
+    Bk::sync();
+    BankOffer r = S.ex[par][0];
+#pragma unroll
+    for (int i = 1; i < NW; ++i) {
+      const BankOffer& x = S.ex[par][i];
+      if (x.has && (!r.has || less_pk(x.p, x.k, r.p, r.k))) {
+        r.p = x.p;
+        r.k = x.k;
+        r.has = 1;
+        r.slot = x.slot;
+        r.rb = x.rb;
+        r.deg = x.deg;
+      }
+      r.fresh += x.fresh;
+      r.nimp += x.nimp;
+      r.nq += x.nq;
+      r.flags |= x.flags;
+    }
+    return r;
+  }
+};
+
+// par_dijkstra with one CTA (NW warps) per source and a banked level 0.
+template <int NW, int KI, int VT>
+__global__ void __launch_bounds__(32 * NW, 1)
+    k_sssp_bank(pbh_heap_dev* heaps, const u64* __restrict__ off, const u32* __restrict__ tgt,
+                const u32* __restrict__ wt, u32 V, const u32* sources, u64* dist, u32* settled,
+                SsspState* sst, BankL0<32 * NW, KI>* save, u32 dag_mode, u32 max_deg, u32 d) {
+  using BH = BankHeap<NW, KI, VT>;
+  using HC = typename BH::HC;
+  using Bk = Blk<BH::B>;
+  constexpr u32 B = BH::B;
+  constexpr u32 C0 = BH::C0;
+  constexpr u32 PE = BH::PE;
+  BankSmem<NW, KI, VT>& S = bank_smem<NW, KI, VT>();
+  SsspState* my = sst + blockIdx.x;
+  if (my->status != 0 && my->status != 7) return;
+  pbh_heap_dev* g = heaps + blockIdx.x;
+  typename HC::Sm& sm = S.hs;
+  HC hc{sm};
+  hc.load(g, S.bk[0], S.bp[0], S.bk[1], S.bp[1], true);
+  hc.bk = g->g_bk;
+  hc.bp = g->g_bp;
+  hc.pk = g->g_pk;
+  hc.pp = g->g_pp;
+  hc.rm = g->g_rm;
+  hc.bo = nullptr;
+  const u32 tid = threadIdx.x;
+  BankL0<B, KI>& L = S.l0;
+  BH H(hc, S, g->idx, off);
+  pbh_idx_entry* idx = g->idx;
+  u64* my_dist = dist + (u64)blockIdx.x * V;
+  u32* my_settled = settled + (u64)blockIdx.x * V;
+  u64 n_settled = my->n_settled, rounds = my->rounds, ops = my->ops;
+  H.live = hc.s.live;
+  H.pushes = sm.ops;  // persisted push counter (this engine reuses the ops slot)
+  H.after_cold();
+  for (u32 i = tid; i < 2 * B; i += B) (&S.dirty[0][0])[i] = 0;
+
+  if (!my->started) {
+    if (tid == 0) {
+      L.qn = 0;
+      L.spl_inf = 1;
+      L.spl_p = 0;
+      L.spl_k = 0;
+      const u32 s = sources[blockIdx.x];
+      pbh_idx_entry e;
+      e.prio = 0;
+      e.state = PBH_ST_LIVE;
+      e.parent = s;
+      idx[s] = e;
+      S.bk[0][0] = s;
+      S.bp[0][0] = 0;
+    }
+    H.rebuild(S.bk[0], S.bp[0], 1);  // eng.update({s, 0}) (sssp.cpp:36)
+    H.live = 1;
+    ops = 1;
+  } else {
+    // resume after NEED_GROW: reload the level-0 image
+    const u32* src = reinterpret_cast<const u32*>(save + blockIdx.x);
+    u32* dst = reinterpret_cast<u32*>(&L);
+    for (u32 i = tid; i < sizeof(BankL0<B, KI>) / 4; i += B) dst[i] = src[i];
+    Bk::sync();
+    H.occm = L.occ[tid];
+    H.rescan();
+  }
+  H.qn = L.qn;
+  Bk::sync();
+
+  bool need_grow = false;
+  const u32 Lnl = sm.n_levels;
+  const u64 cap_last = Lnl == 1 ? (u64)sm.cap0 : sm.lv[Lnl - 1].cap_b;
+  u32 par = 0;                   // exchange parity
+  bool rescan_due = false;       // this thread's bank minimum is stale
+  bool evict_due = false;        // replicated: some bank lacks room for a pass
+  // the next extraction, when known from the previous round's exchange
+  bool nx = false;
+  BankOffer cur{};
+  u32 pu[PE], pw[PE];  // its row's first pass (prefetched)
+  while (!hc.failed() && H.live > 0) {
+    if ((u64)C0 + H.qn + H.deep_n + max_deg + kBankQ + C0 > cap_last) {
+      need_grow = true;
+      break;
+    }
+    const bool hit = nx;
+    if (!nx) {
+      // ---- extract_min: CTA argmin of the bank minima
+      if (rescan_due) H.rescan();
+      rescan_due = false;
+      cur = H.exchange(par, H.lhas, H.lmin_p, H.lmin_k, H.lmin_s,
+                       H.lhas ? L.lrb[H.lmin_s] : 0, H.lhas ? L.ldeg[H.lmin_s] : 0, 0, 0, 0, 0);
+      par ^= 1;
+      if (!cur.has) {
+        H.refill();
+        if (hc.failed()) break;
+        if (H.n_l0 == 0) {
+          hc.fail(PBH_ERR_INVARIANT, 0xE5);
+          break;
+        }
+        evict_due = false;
+        continue;
+      }
+    }
+    nx = false;
+    const u64 p = cur.p;
+    const u32 v = cur.k;
+    if (cur.slot % B == tid) {
+      H.occm &= ~(1u << (cur.slot / B));
+      rescan_due = true;
+    }
+    const u32 rot = (u32)n_settled & (B - 1);  // edge j of a pass -> thread (j - rot) mod B
+    if (tid == 0) {
+      idx[v].state = PBH_ST_DEAD;
+      my_dist[v] = p;
+      my_settled[n_settled] = v;
+    }
+    ++n_settled;
+    ++rounds;
+    ++ops;
+    --H.live;
+    // ---- relax the row in passes of 256 edges (sssp.cpp:49-57)
+    u32 n_imp = 0;
+    bool fail_bad = false, fail_ovf = false;
+    const u64 rb = cur.rb, re = cur.rb + cur.deg;
+    const u32 te = (tid + rot) & (B - 1);  // this thread's edge offset within a group of B
+    for (u64 base = rb; base < re; base += kBankPass) {
+      const bool last = base + kBankPass >= re;
+      const u32 rem = (u32)(re - base);
+      if (evict_due) {
+        H.evict();
+        rescan_due = false;
+        evict_due = false;
+        if (hc.failed()) break;
+      }
+      if (H.qn > (u32)(kBankQ - kBankPass)) {
+        H.flush_q();
+        if (hc.failed()) break;
+      }
+      u32 uu[PE], ww[PE];
+      if (hit && base == rb) {
+#pragma unroll
+        for (u32 t = 0; t < PE; ++t) {
+          uu[t] = pu[t];
+          ww[t] = pw[t];
+        }
+      } else {
+#pragma unroll
+        for (u32 t = 0; t < PE; ++t) {
+          const bool in = te + B * t < rem;
+          uu[t] = in ? __ldg(tgt + base + te + B * t) : 0;
+          ww[t] = in ? __ldg(wt + base + te + B * t) : 0;
+        }
+      }
+      ulonglong2 ee[PE];
+      u64 ob[PE], oe[PE];
+#pragma unroll
+      for (u32 t = 0; t < PE; ++t) {
+        ee[t] = make_ulonglong2(~0ull, PBH_ST_DEAD);
+        ob[t] = oe[t] = 0;
+        if (te + B * t < rem) {
+          ee[t] = __ldcg(reinterpret_cast<const ulonglong2*>(idx + uu[t]));
+          ob[t] = __ldg(off + uu[t]);
+          oe[t] = __ldg(off + uu[t] + 1);
+        }
+      }
+      // deferred rescans (extraction owner, decreased banks) under the gathers
+      if (rescan_due) H.rescan();
+      rescan_due = false;
+      // ---- candidates, applied by the relaxing thread
+      u32 fresh = 0, nimp = 0, nq = 0;
+      bool ovf = false, bad = false;
+      bool ch = false;
+      u64 cbp = 0, cbrb = 0;
+      u32 cbk = 0, cbs = 0, cbd = 0;
+#pragma unroll
+      for (u32 t = 0; t < PE; ++t) {
+        const u32 st = (u32)ee[t].y;
+        const u64 c = p + ww[t];
+        if (!(te + B * t < rem) || (!dag_mode && PBH_ST(st) == PBH_ST_DEAD)) continue;
+        ovf |= c < p;
+        if (!(c < ee[t].x)) continue;
+        const u32 u = uu[t];
+        ++nimp;
+        fresh += PBH_ST(st) != PBH_ST_LIVE;
+        const u32 loc = st >> 2;
+        u32 nst, sl = 0;
+        bool admitted = true;
+        if (PBH_ST(st) == PBH_ST_LIVE && loc < C0) {
+          // decrease in place; the owner rescans next pass
+          bad |= !(L.lk[loc] == u && L.lp[loc] == ee[t].x);
+          L.lp[loc] = c;
+          S.dirty[par][loc % B] = 1;
+          nst = st;
+          sl = loc;
+        } else if (H.adm(c, u)) {
+          const u32 i = __ffs(~H.occm) - 1;
+          sl = i * B + tid;
+          H.occm |= 1u << i;
+          L.lk[sl] = u;
+          L.lp[sl] = c;
+          L.lrb[sl] = ob[t];
+          L.ldeg[sl] = (u32)(oe[t] - ob[t]);
+          if (!H.lhas || less_pk(c, u, H.lmin_p, H.lmin_k)) {
+            H.lhas = true;
+            H.lmin_p = c;
+            H.lmin_k = u;
+            H.lmin_s = sl;
+          }
+          nst = PBH_ST_LIVE | (sl << 2);
+        } else {
+          const u32 qp_ = atomicAdd(&L.qn, 1u);
+          L.qk[qp_] = u;
+          L.qp[qp_] = c;
+          ++nq;
+          admitted = false;
+          nst = PBH_ST_LIVE | (PBH_LOC_DEEP << 2);
+        }
+        if (admitted && (!ch || less_pk(c, u, cbp, cbk))) {
+          ch = true;
+          cbp = c;
+          cbk = u;
+          cbs = sl;
+          cbrb = ob[t];
+          cbd = (u32)(oe[t] - ob[t]);
+        }
+        pbh_idx_entry e;
+        e.prio = c;
+        e.state = nst;
+        e.parent = v;
+        reinterpret_cast<ulonglong2*>(idx)[u] = *reinterpret_cast<const ulonglong2*>(&e);
+      }
+      // ---- exchange: this thread offers min(bank minimum, best candidate)
+      bool oh = H.lhas;
+      u64 op = H.lmin_p;
+      u32 ok = H.lmin_k, os = H.lmin_s;
+      u64 orb = cbrb;
+      u32 od = cbd;
+      if (ch && (!oh || less_pk(cbp, cbk, op, ok))) {
+        oh = true;
+        op = cbp;
+        ok = cbk;
+        os = cbs;
+      } else if (oh) {
+        orb = L.lrb[os];
+        od = L.ldeg[os];
+      }
+      const u32 flags = ((u32)__popc(H.occm) > (u32)KI - PE ? 1u : 0u) | (bad ? 2u : 0u) |
+                        (ovf ? 4u : 0u);
+      const BankOffer r = H.exchange(par, oh, op, ok, os, orb, od, fresh, nimp, nq, flags);
+      if (S.dirty[par][tid]) {
+        S.dirty[par][tid] = 0;
+        rescan_due = true;
+      }
+      par ^= 1;
+      n_imp += r.nimp;
+      H.live += r.fresh;
+      H.qn += r.nq;
+      evict_due = (r.flags & 1u) != 0;
+      fail_bad |= (r.flags & 2u) != 0;
+      fail_ovf |= (r.flags & 4u) != 0;
+      if (fail_bad || fail_ovf) break;
+      if (last && r.has) {
+        // the next extraction: load its row's first pass now
+        nx = true;
+        cur = r;
+        const u32 te2 = (tid + rot + 1) & (B - 1);
+#pragma unroll
+        for (u32 t = 0; t < PE; ++t) {
+          const u32 j = te2 + B * t;
+          pu[t] = j < r.deg ? __ldg(tgt + r.rb + j) : 0;
+          pw[t] = j < r.deg ? __ldg(wt + r.rb + j) : 0;
+        }
+      }
+    }
+    if (hc.failed()) break;
+    if (fail_bad) {
+      hc.fail(PBH_ERR_INVARIANT, 0xD1);
+      break;
+    }
+    if (fail_ovf) {
+      hc.fail(PBH_ERR_OVERFLOW, v);
+      break;
+    }
+    ops += n_imp <= d ? (n_imp != 0) : (n_imp + d - 1) / d;  // bulk_update batches of <= d
+  }
+  // persist the level-0 image (a NEED_GROW relaunch resumes from it)
+  Bk::sync();
+  L.occ[tid] = H.occm;
+  if (tid == 0) L.qn = H.qn;
+  Bk::sync();
+  {
+    const u32* src = reinterpret_cast<const u32*>(&L);
+    u32* dst = reinterpret_cast<u32*>(save + blockIdx.x);
+    for (u32 i = tid; i < sizeof(BankL0<B, KI>) / 4; i += B) dst[i] = src[i];
+  }
+  H.to_cold();
+  if (tid == 0) sm.ops = H.pushes;
+  Bk::sync();
+  hc.store();
+  if (tid == 0) {
+    my->n_settled = n_settled;
+    my->rounds = rounds;
+    my->started = 1;
+    my->ops = ops;
+    if (need_grow && !hc.failed()) {
+      my->status = 7;
+    } else {
+      my->status = sm.status;
+      my->detail = sm.detail;
+    }
+  }
+}
+
+}  // namespace pbh_dev

@@ -14,6 +14,7 @@
 
 #include "../../include/pbh_gpu.h"
 #include "pbh_fast.cuh"
+#include "pbh_bank.cuh"
 
 using namespace pbh_dev;
 
@@ -181,6 +182,56 @@ cudaError_t launch_sssp_fast(const FastLayout& L, cudaStream_t st, u32 grid, pbh
   fn<<<grid, 32, 0, st>>>(heaps, off, tgt, w, V, src, dist, settled, sst, dag, maxdeg, d, L, xp);
   g_launches++;
   return cudaGetLastError();
+}
+
+// Banked level-0 SSSP engine variants: NW warps per source, KI slots per
+// thread, level 0 = 32*NW*KI = 1024 slots.
+template <int NW>
+struct BankCfg;
+template <>
+struct BankCfg<1> { static constexpr int KI = 32; };
+template <>
+struct BankCfg<4> { static constexpr int KI = 8; };
+template <>
+struct BankCfg<8> { static constexpr int KI = 4; };
+constexpr int kBankC0 = 1024;
+
+template <int NW>
+size_t bank_save_bytes() {
+  return sizeof(BankL0<32 * NW, BankCfg<NW>::KI>);
+}
+size_t bank_save_bytes_nw(int nw) {
+  return nw == 1 ? bank_save_bytes<1>() : nw == 4 ? bank_save_bytes<4>() : bank_save_bytes<8>();
+}
+
+template <int NW>
+cudaError_t launch_sssp_bank(cudaStream_t st, u32 grid, pbh_heap_dev* heaps, const u64* off,
+                             const u32* tgt, const u32* w, u32 V, const u32* src, u64* dist,
+                             u32* settled, SsspState* sst, void* save, u32 dag, u32 maxdeg, u32 d) {
+  constexpr int KI = BankCfg<NW>::KI;
+  auto fn = k_sssp_bank<NW, KI, VT>;
+  const int smem = (int)sizeof(BankSmem<NW, KI, VT>);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  fn<<<grid, 32 * NW, smem, st>>>(heaps, off, tgt, w, V, src, dist, settled, sst,
+                                  reinterpret_cast<BankL0<32 * NW, KI>*>(save), dag, maxdeg, d);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sssp_bank_nw(int nw, cudaStream_t st, u32 grid, pbh_heap_dev* heaps,
+                                const u64* off, const u32* tgt, const u32* w, u32 V,
+                                const u32* src, u64* dist, u32* settled, SsspState* sst,
+                                void* save, u32 dag, u32 maxdeg, u32 d) {
+  switch (nw) {
+    case 1: return launch_sssp_bank<1>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
+    case 4: return launch_sssp_bank<4>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
+    default: return launch_sssp_bank<8>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
+  }
 }
 
 __global__ void k_finalize_parent(const pbh_idx_entry* idx, u32 V, u32* parent) {
@@ -831,7 +882,10 @@ struct pbh_sssp_ctx {
   u64 max_sources = 0;
   SmLayout layout{};
   FastLayout flayout{};
-  bool fast = true;
+  bool fast = true;   // warp engines (lane-banked or sorted-B_0); false = CTA engine
+  bool lane = true;   // banked level 0 (default)
+  int bank_nw = 1;    // warps per source of the banked engine
+  void* d_save = nullptr;
   std::vector<DevHeap> heaps;
   pbh_heap_dev* d_heaps = nullptr;
   SsspState* d_sst = nullptr;
@@ -908,8 +962,17 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
   c->d = std::min<u64>(c->d, std::max<u64>(1, md ? md : 1));  // batches never exceed a row
   c->nt = pick_nt(std::max<u64>(c->d, std::min<u64>(md, 1024)));
   c->cap0 = pick_cap0(c->d);
-  if (const char* e = getenv("PBH_SSSP_ENGINE")) c->fast = std::string(e) != "cta";
-  if (c->fast) {
+  if (const char* e = getenv("PBH_SSSP_ENGINE")) {
+    c->fast = std::string(e) != "cta";
+    c->lane = std::string(e) == "lane";
+  }
+  if (c->lane) {
+    c->bank_nw = 4;
+    if (const char* e = getenv("PBH_SSSP_NW")) c->bank_nw = atoi(e);
+    if (c->bank_nw != 1 && c->bank_nw != 4 && c->bank_nw != 8) c->bank_nw = 4;
+    c->cap0 = kBankC0 / 2;
+    c->nt = 32 * c->bank_nw;
+  } else if (c->fast) {
     c->cap0 = kFastCap0;
     c->nt = 32;
     c->flayout = make_fast_layout(c->cap0);
@@ -922,6 +985,9 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
   if ((st = ctx_alloc(c, (void**)&c->d_settled, max_sources * c->V * 4))) return fail(st);
   if ((st = ctx_alloc(c, (void**)&c->d_parent, max_sources * c->V * 4))) return fail(st);
   if ((st = ctx_alloc(c, (void**)&c->d_src, max_sources * 4))) return fail(st);
+  if (c->lane &&
+      (st = ctx_alloc(c, (void**)&c->d_save, max_sources * bank_save_bytes_nw(c->bank_nw))))
+    return fail(st);
   c->heaps.resize(max_sources);
   // initial levels: enough for a few rows of relaxations
   u32 nlev = 2;
@@ -974,7 +1040,12 @@ pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n
   std::vector<SsspState> hs(n_sources);
   for (int guard = 0; guard < 256; ++guard) {
     CK(cudaEventRecord(c->ev0, c->stream));
-    if (c->fast) {
+    if (c->lane) {
+      CK(launch_sssp_bank_nw(c->bank_nw, c->stream, (u32)n_sources, c->d_heaps, c->d_off,
+                             c->d_tgt, c->d_w, c->V, c->d_src, c->d_dist, c->d_settled, c->d_sst,
+                             c->d_save, dag_mode ? 1 : 0, c->max_deg,
+                             (u32)std::min<u64>(c->d, 0xffffffffu)));
+    } else if (c->fast) {
       CK(launch_sssp_fast(c->flayout, c->stream, (u32)n_sources, c->d_heaps, c->d_off, c->d_tgt,
                           c->d_w, c->V, c->d_src, c->d_dist, c->d_settled, c->d_sst,
                           dag_mode ? 1 : 0, c->max_deg, (u32)std::min<u64>(c->d, 0xffffffffu)));
@@ -1020,6 +1091,10 @@ pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n
     SsspState s0;
     cudaMemcpy(&s0, c->d_sst, sizeof s0, cudaMemcpyDeviceToHost);
     const double r = s0.rounds ? (double)s0.rounds : 1.0;
+    if (c->lane)
+      fprintf(stderr, "phases cyc/round (lane): extract %.0f relax %.0f apply %.0f cold %.0f tail %.0f\n",
+              s0.phase[0] / r, s0.phase[1] / r, s0.phase[2] / r, s0.phase[3] / r, s0.phase[4] / r);
+    else
     fprintf(stderr, "phases cyc/round: extract %.0f relax %.0f kill %.0f append %.0f tail %.0f | flush %.0f (n=%llu) smin %.0f | pf_hits %.3f\n",
             s0.phase[0] / r, s0.phase[1] / r, s0.phase[2] / r, s0.phase[3] / r, s0.phase[4] / r,
             s0.phase[5] / r, (unsigned long long)s0.pad2, s0.phase[6] / r, s0.phase[7] / r);
