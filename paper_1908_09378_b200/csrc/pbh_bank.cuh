@@ -74,6 +74,8 @@ struct BankSmem {
   // it is also the sort scratch of evict()
   u32 bk[2][C0 / 2];
   u64 bp[2][C0 / 2];
+  u32 pf_t[kBankPass];  // next row's first pass, prefetched by cp.async
+  u32 pf_w[kBankPass];
   BankOffer ex[2][NW];  // per-pass exchange (parity double-buffered)
   u8 dirty[2][B];       // decreased-bank flags (parity double-buffered)
   HeapSmem<B, VT> hs;
@@ -84,6 +86,24 @@ DEV BankSmem<NW, KI, VT>& bank_smem() {
   extern __shared__ __align__(16) unsigned char dyn[];
   return *reinterpret_cast<BankSmem<NW, KI, VT>*>(dyn);
 }
+
+// 4-byte global -> shared copy that bypasses registers (zero-fill when !pred).
+DEV void cp_async4(void* smem, const void* gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(pred ? 4 : 0)
+               : "memory");
+}
+// Bulk L2 prefetch of the 4-byte array range [a[i0], a[i1]) (16-byte granular).
+DEV void l2_prefetch_range(const u32* a, u64 i0, u64 i1) {
+  const u64 b0 = (reinterpret_cast<u64>(a + i0)) & ~15ull;
+  const u64 b1 = (reinterpret_cast<u64>(a + i1) + 15) & ~15ull;
+  if (b1 > b0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(b0), "r"((u32)(b1 - b0))
+                 : "memory");
+}
+DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // warp argmin of (p, k) over lanes with `has`; returns the winning lane.
 DEV u32 warp_argmin(bool& has, u64& p, u32& k) {
@@ -99,6 +119,110 @@ DEV u32 warp_argmin(bool& has, u64& p, u32& k) {
   p = ((u64)mhi << 32) | mlo;
   k = mk;
   return win ? __ffs(win) - 1 : 0;
+}
+
+// This thread's bank minimum (inline on kernel locals so they stay in registers).
+template <int B, int KI>
+DEV void bank_rescan(const BankL0<B, KI>& L, u32 tid, u32 occm, bool& lhas, u64& lmin_p,
+                     u32& lmin_k, u32& lmin_s) {
+  lhas = false;
+  u32 m = occm;
+  while (m) {
+    const u32 i = __ffs(m) - 1;
+    m &= m - 1;
+    const u32 s = i * B + tid;
+    const u64 p = L.lp[s];
+    const u32 k = L.lk[s];
+    if (!lhas || less_pk(p, k, lmin_p, lmin_k)) {
+      lhas = true;
+      lmin_p = p;
+      lmin_k = k;
+      lmin_s = s;
+    }
+  }
+}
+
+template <int NW, int KI, int VT>
+struct BankSmem;
+template <int NW, int KI, int VT>
+DEV BankSmem<NW, KI, VT>& bank_smem();
+
+// Per-pass exchange: CTA argmin of the offers (has, p, k) with their slot
+// and row, and the sums of the counters. One barrier. Counters are packed
+// 9 bits each (every one is <= 256 per pass): c0 = fresh | nimp << 9 |
+// ovf << 18, c1 = nq | evict << 9 | bad << 18 (the last two per-thread flags).
+template <int NW, int KI, int VT>
+DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u32 deg, u32 c0,
+                            u32 c1) {
+  BankSmem<NW, KI, VT>& S = bank_smem<NW, KI, VT>();
+  const u32 tid = threadIdx.x;
+  const u32 lane = tid & 31, w = tid >> 5;
+  bool h = has;
+  u64 wp = p;
+  u32 wk = k;
+  const u32 wl = warp_argmin(h, wp, wk);
+  const u32 s0 = __reduce_add_sync(0xffffffffu, c0);
+  const u32 s1 = __reduce_add_sync(0xffffffffu, c1);
+  if (lane == wl) {
+    BankOffer& o = S.ex[par][w];
+    o.p = wp;
+    o.k = wk;
+    o.has = h;
+    o.slot = slot;
+    o.rb = rb;
+    o.deg = deg;
+    o.fresh = s0;
+    o.nq = s1;
+  }
+  if constexpr (NW == 1) {
+    __syncwarp();
+    BankOffer r;
+    r.p = wp;
+    r.k = wk;
+    r.has = h;
+    r.slot = __shfl_sync(0xffffffffu, slot, wl);
+    r.rb = __shfl_sync(0xffffffffu, rb, wl);
+    r.deg = __shfl_sync(0xffffffffu, deg, wl);
+    r.fresh = s0 & 511u;
+    r.nimp = (s0 >> 9) & 511u;
+    r.nq = s1 & 511u;
+    r.flags = ((s1 >> 9) & 511u ? 1u : 0u) | ((s1 >> 18) & 511u ? 2u : 0u) | ((s0 >> 18) & 511u ? 4u : 0u);
+    return r;
+  } else {
+    __syncthreads();
+    // tree argmin over the NW warp winners (index only), then one read
+    u32 bi = 0;
+    bool bh = S.ex[par][0].has;
+    u64 bp = S.ex[par][0].p;
+    u32 bk = S.ex[par][0].k;
+    u32 t0 = S.ex[par][0].fresh, t1 = S.ex[par][0].nq;
+#pragma unroll
+    for (int i = 1; i < NW; ++i) {
+      const bool xh = S.ex[par][i].has;
+      const u64 xp = S.ex[par][i].p;
+      const u32 xk = S.ex[par][i].k;
+      t0 += S.ex[par][i].fresh;
+      t1 += S.ex[par][i].nq;
+      if (xh && (!bh || less_pk(xp, xk, bp, bk))) {
+        bh = true;
+        bp = xp;
+        bk = xk;
+        bi = i;
+      }
+    }
+    BankOffer r;
+    r.p = bp;
+    r.k = bk;
+    r.has = bh;
+    r.slot = S.ex[par][bi].slot;
+    r.rb = S.ex[par][bi].rb;
+    r.deg = S.ex[par][bi].deg;
+    r.fresh = t0 & 511u;
+    r.nimp = (t0 >> 9) & 511u;
+    r.nq = t1 & 511u;
+    r.flags = ((t1 >> 9) & 511u ? 1u : 0u) | ((t1 >> 18) & 511u ? 2u : 0u) | ((t0 >> 18) & 511u ? 4u : 0u);
+    return r;
+  }
 }
 
 template <int NW, int KI, int VT>
@@ -276,55 +400,11 @@ struct BankHeap {
     after_cold();
   }
 
-  // Per-pass exchange: CTA argmin of the offers (has, p, k) with their slot
-  // and row, and sums of the counters. One barrier.
-  DEV BankOffer exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u32 deg, u32 fresh,
-                         u32 nimp, u32 nq, u32 flags) {
-    const u32 lane = tid & 31, w = tid >> 5;
-    bool h = has;
-    u64 wp = p;
-    u32 wk = k;
-    const u32 wl = warp_argmin(h, wp, wk);
-    const u32 sf = __reduce_add_sync(0xffffffffu, fresh);
-    const u32 sn = __reduce_add_sync(0xffffffffu, nimp);
-    const u32 sq = __reduce_add_sync(0xffffffffu, nq);
-    const u32 fl = __reduce_or_sync(0xffffffffu, flags);
-    BankOffer& o = S.ex[par][w];
-    if (lane == wl) {
-      o.p = wp;
-      o.k = wk;
-      o.has = h;
-      o.slot = slot;
-      o.rb = rb;
-      o.deg = deg;
-      o.fresh = sf;
-      o.nimp = sn;
-      o.nq = sq;
-      o.flags = fl;
-    }
-    Bk::sync();
-    BankOffer r = S.ex[par][0];
-#pragma unroll
-    for (int i = 1; i < NW; ++i) {
-      const BankOffer& x = S.ex[par][i];
-      if (x.has && (!r.has || less_pk(x.p, x.k, r.p, r.k))) {
-        r.p = x.p;
-        r.k = x.k;
-        r.has = 1;
-        r.slot = x.slot;
-        r.rb = x.rb;
-        r.deg = x.deg;
-      }
-      r.fresh += x.fresh;
-      r.nimp += x.nimp;
-      r.nq += x.nq;
-      r.flags |= x.flags;
-    }
-    return r;
-  }
 };
 
 // par_dijkstra with one CTA (NW warps) per source and a banked level 0.
+// The hot loop keeps all state in locals (registers); the BankHeap object is
+// only the hand-off to the cold-path methods.
 template <int NW, int KI, int VT>
 __global__ void __launch_bounds__(32 * NW, 1)
     k_sssp_bank(pbh_heap_dev* heaps, const u64* __restrict__ off, const u32* __restrict__ tgt,
@@ -352,7 +432,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
   const u32 tid = threadIdx.x;
   BankL0<B, KI>& L = S.l0;
   BH H(hc, S, g->idx, off);
-  pbh_idx_entry* idx = g->idx;
+  pbh_idx_entry* const idx = g->idx;
   u64* my_dist = dist + (u64)blockIdx.x * V;
   u32* my_settled = settled + (u64)blockIdx.x * V;
   u64 n_settled = my->n_settled, rounds = my->rounds, ops = my->ops;
@@ -391,31 +471,62 @@ __global__ void __launch_bounds__(32 * NW, 1)
   H.qn = L.qn;
   Bk::sync();
 
+  // ---- hot state in registers
+  u32 occm = H.occm;
+  bool lhas = H.lhas;
+  u64 lmin_p = H.lmin_p;
+  u32 lmin_k = H.lmin_k, lmin_s = H.lmin_s;
+  i64 live = H.live;
+  u32 qn = H.qn;
+  u64 deep_n = H.deep_n;
+#define BANK_TO_H()     \
+  H.occm = occm;        \
+  H.lhas = lhas;        \
+  H.lmin_p = lmin_p;    \
+  H.lmin_k = lmin_k;    \
+  H.lmin_s = lmin_s;    \
+  H.live = live;        \
+  H.qn = qn;            \
+  H.deep_n = deep_n;
+#define BANK_FROM_H()   \
+  occm = H.occm;        \
+  lhas = H.lhas;        \
+  lmin_p = H.lmin_p;    \
+  lmin_k = H.lmin_k;    \
+  lmin_s = H.lmin_s;    \
+  live = H.live;        \
+  qn = H.qn;            \
+  deep_n = H.deep_n;
+
   bool need_grow = false;
   const u32 Lnl = sm.n_levels;
   const u64 cap_last = Lnl == 1 ? (u64)sm.cap0 : sm.lv[Lnl - 1].cap_b;
-  u32 par = 0;                   // exchange parity
-  bool rescan_due = false;       // this thread's bank minimum is stale
-  bool evict_due = false;        // replicated: some bank lacks room for a pass
-  // the next extraction, when known from the previous round's exchange
-  bool nx = false;
+  const u64 grow_at = cap_last - ((u64)2 * C0 + max_deg + kBankQ);  // NEED_GROW threshold
+  const bool grow_ok = cap_last > (u64)2 * C0 + max_deg + kBankQ;
+  u32 par = 0;                // exchange parity
+  bool rescan_due = false;    // this thread's bank minimum is stale
+  bool evict_due = false;     // replicated: some bank lacks room for a pass
+  bool nx = false;            // the next extraction is known (cur)
   BankOffer cur{};
-  u32 pu[PE], pw[PE];  // its row's first pass (prefetched)
-  while (!hc.failed() && H.live > 0) {
-    if ((u64)C0 + H.qn + H.deep_n + max_deg + kBankQ + C0 > cap_last) {
+  bool fail_bad = false, fail_ovf = false;
+  u32 fail_v = 0;
+  while (live > 0) {
+    if (!grow_ok || (u64)qn + deep_n > grow_at) {
       need_grow = true;
       break;
     }
     const bool hit = nx;
     if (!nx) {
       // ---- extract_min: CTA argmin of the bank minima
-      if (rescan_due) H.rescan();
+      if (rescan_due) bank_rescan<B, KI>(L, tid, occm, lhas, lmin_p, lmin_k, lmin_s);
       rescan_due = false;
-      cur = H.exchange(par, H.lhas, H.lmin_p, H.lmin_k, H.lmin_s,
-                       H.lhas ? L.lrb[H.lmin_s] : 0, H.lhas ? L.ldeg[H.lmin_s] : 0, 0, 0, 0, 0);
+      cur = bank_exchange<NW, KI, VT>(par, lhas, lmin_p, lmin_k, lmin_s,
+                                      lhas ? L.lrb[lmin_s] : 0, lhas ? L.ldeg[lmin_s] : 0, 0, 0);
       par ^= 1;
       if (!cur.has) {
+        BANK_TO_H();
         H.refill();
+        BANK_FROM_H();
         if (hc.failed()) break;
         if (H.n_l0 == 0) {
           hc.fail(PBH_ERR_INVARIANT, 0xE5);
@@ -429,7 +540,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
     const u64 p = cur.p;
     const u32 v = cur.k;
     if (cur.slot % B == tid) {
-      H.occm &= ~(1u << (cur.slot / B));
+      occm &= ~(1u << (cur.slot / B));
       rescan_due = true;
     }
     const u32 rot = (u32)n_settled & (B - 1);  // edge j of a pass -> thread (j - rot) mod B
@@ -441,31 +552,36 @@ __global__ void __launch_bounds__(32 * NW, 1)
     ++n_settled;
     ++rounds;
     ++ops;
-    --H.live;
+    --live;
     // ---- relax the row in passes of 256 edges (sssp.cpp:49-57)
     u32 n_imp = 0;
-    bool fail_bad = false, fail_ovf = false;
-    const u64 rb = cur.rb, re = cur.rb + cur.deg;
+    const u64 rb = cur.rb;
+    const u32 deg = cur.deg;
     const u32 te = (tid + rot) & (B - 1);  // this thread's edge offset within a group of B
-    for (u64 base = rb; base < re; base += kBankPass) {
-      const bool last = base + kBankPass >= re;
-      const u32 rem = (u32)(re - base);
-      if (evict_due) {
-        H.evict();
-        rescan_due = false;
+    bool cold_fail = false;
+    for (u32 done = 0; done < deg; done += kBankPass) {
+      const bool last = done + kBankPass >= deg;
+      const u32 rem = deg - done;
+      const u64 base = rb + done;
+      if (evict_due || qn > (u32)(kBankQ - kBankPass)) {
+        BANK_TO_H();
+        if (evict_due) H.evict();
+        if (!hc.failed() && H.qn > (u32)(kBankQ - kBankPass)) H.flush_q();
+        BANK_FROM_H();
+        if (evict_due) rescan_due = false;
         evict_due = false;
-        if (hc.failed()) break;
-      }
-      if (H.qn > (u32)(kBankQ - kBankPass)) {
-        H.flush_q();
-        if (hc.failed()) break;
+        if (hc.failed()) {
+          cold_fail = true;
+          break;
+        }
       }
       u32 uu[PE], ww[PE];
-      if (hit && base == rb) {
+      if (hit && done == 0) {
+        cp_async_wait_all();
 #pragma unroll
         for (u32 t = 0; t < PE; ++t) {
-          uu[t] = pu[t];
-          ww[t] = pw[t];
+          uu[t] = S.pf_t[t * B + tid];
+          ww[t] = S.pf_w[t * B + tid];
         }
       } else {
 #pragma unroll
@@ -487,8 +603,9 @@ __global__ void __launch_bounds__(32 * NW, 1)
           oe[t] = __ldg(off + uu[t] + 1);
         }
       }
+      asm volatile("" ::: "memory");  // issue the gathers before the rescans' shared loads
       // deferred rescans (extraction owner, decreased banks) under the gathers
-      if (rescan_due) H.rescan();
+      if (rescan_due) bank_rescan<B, KI>(L, tid, occm, lhas, lmin_p, lmin_k, lmin_s);
       rescan_due = false;
       // ---- candidates, applied by the relaxing thread
       u32 fresh = 0, nimp = 0, nq = 0;
@@ -516,21 +633,27 @@ __global__ void __launch_bounds__(32 * NW, 1)
           S.dirty[par][loc % B] = 1;
           nst = st;
           sl = loc;
-        } else if (H.adm(c, u)) {
-          const u32 i = __ffs(~H.occm) - 1;
+        } else if (L.spl_inf || c < L.spl_p || (c == L.spl_p && u <= L.spl_k)) {
+          const u32 i = __ffs(~occm) - 1;
           sl = i * B + tid;
-          H.occm |= 1u << i;
+          occm |= 1u << i;
           L.lk[sl] = u;
           L.lp[sl] = c;
           L.lrb[sl] = ob[t];
           L.ldeg[sl] = (u32)(oe[t] - ob[t]);
-          if (!H.lhas || less_pk(c, u, H.lmin_p, H.lmin_k)) {
-            H.lhas = true;
-            H.lmin_p = c;
-            H.lmin_k = u;
-            H.lmin_s = sl;
+          if (!lhas || less_pk(c, u, lmin_p, lmin_k)) {
+            lhas = true;
+            lmin_p = c;
+            lmin_k = u;
+            lmin_s = sl;
           }
           nst = PBH_ST_LIVE | (sl << 2);
+          if (PBH_ST(st) != PBH_ST_LIVE) {
+            // first sighting of a vertex that may be extracted soon: pull its
+            // row into L2 so its first pass loads at L2 latency
+            l2_prefetch_range(tgt, ob[t], oe[t]);
+            l2_prefetch_range(wt, ob[t], oe[t]);
+          }
         } else {
           const u32 qp_ = atomicAdd(&L.qn, 1u);
           L.qk[qp_] = u;
@@ -554,9 +677,9 @@ __global__ void __launch_bounds__(32 * NW, 1)
         reinterpret_cast<ulonglong2*>(idx)[u] = *reinterpret_cast<const ulonglong2*>(&e);
       }
       // ---- exchange: this thread offers min(bank minimum, best candidate)
-      bool oh = H.lhas;
-      u64 op = H.lmin_p;
-      u32 ok = H.lmin_k, os = H.lmin_s;
+      bool oh = lhas;
+      u64 op = lmin_p;
+      u32 ok = lmin_k, os = lmin_s;
       u64 orb = cbrb;
       u32 od = cbd;
       if (ch && (!oh || less_pk(cbp, cbk, op, ok))) {
@@ -568,21 +691,25 @@ __global__ void __launch_bounds__(32 * NW, 1)
         orb = L.lrb[os];
         od = L.ldeg[os];
       }
-      const u32 flags = ((u32)__popc(H.occm) > (u32)KI - PE ? 1u : 0u) | (bad ? 2u : 0u) |
-                        (ovf ? 4u : 0u);
-      const BankOffer r = H.exchange(par, oh, op, ok, os, orb, od, fresh, nimp, nq, flags);
+      const u32 ev = (u32)__popc(occm) > (u32)KI - PE ? 1u : 0u;
+      const BankOffer r = bank_exchange<NW, KI, VT>(
+          par, oh, op, ok, os, orb, od, fresh | (nimp << 9) | ((ovf ? 1u : 0u) << 18),
+          nq | (ev << 9) | ((bad ? 1u : 0u) << 18));
       if (S.dirty[par][tid]) {
         S.dirty[par][tid] = 0;
         rescan_due = true;
       }
       par ^= 1;
       n_imp += r.nimp;
-      H.live += r.fresh;
-      H.qn += r.nq;
+      live += r.fresh;
+      qn += r.nq;
       evict_due = (r.flags & 1u) != 0;
-      fail_bad |= (r.flags & 2u) != 0;
-      fail_ovf |= (r.flags & 4u) != 0;
-      if (fail_bad || fail_ovf) break;
+      if (r.flags & 6u) {
+        fail_bad = (r.flags & 2u) != 0;
+        fail_ovf = (r.flags & 4u) != 0;
+        fail_v = v;
+        break;
+      }
       if (last && r.has) {
         // the next extraction: load its row's first pass now
         nx = true;
@@ -591,22 +718,23 @@ __global__ void __launch_bounds__(32 * NW, 1)
 #pragma unroll
         for (u32 t = 0; t < PE; ++t) {
           const u32 j = te2 + B * t;
-          pu[t] = j < r.deg ? __ldg(tgt + r.rb + j) : 0;
-          pw[t] = j < r.deg ? __ldg(wt + r.rb + j) : 0;
+          const bool in = j < r.deg;
+          cp_async4(&S.pf_t[t * B + tid], in ? tgt + r.rb + j : tgt, in);
+          cp_async4(&S.pf_w[t * B + tid], in ? wt + r.rb + j : wt, in);
         }
+        cp_async_commit();
       }
     }
-    if (hc.failed()) break;
-    if (fail_bad) {
-      hc.fail(PBH_ERR_INVARIANT, 0xD1);
-      break;
-    }
-    if (fail_ovf) {
-      hc.fail(PBH_ERR_OVERFLOW, v);
-      break;
-    }
-    ops += n_imp <= d ? (n_imp != 0) : (n_imp + d - 1) / d;  // bulk_update batches of <= d
+    if (cold_fail || fail_bad || fail_ovf) break;
+    // bulk_update batches of <= d (sssp.cpp:59-64)
+    if (n_imp) ops += n_imp <= d ? 1u : (n_imp + d - 1) / d;
   }
+  cp_async_wait_all();
+  BANK_TO_H();
+#undef BANK_TO_H
+#undef BANK_FROM_H
+  if (fail_bad && !hc.failed()) hc.fail(PBH_ERR_INVARIANT, 0xD1);
+  if (fail_ovf && !hc.failed()) hc.fail(PBH_ERR_OVERFLOW, fail_v);
   // persist the level-0 image (a NEED_GROW relaunch resumes from it)
   Bk::sync();
   L.occ[tid] = H.occm;
