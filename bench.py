@@ -6,7 +6,7 @@ SSSP with the bucket-heap par_dijkstra on the dense high-diameter ring band
 (V = 2^20, degree 256, weight-1 spine, seed 2), S = 64 independent sources
 per GPU (weak scaling: rank r solves sources (i*16384 + 257*r) mod V).
 A step = one batched solve of this rank's S sources; each source runs as one
-persistent CTA (k_sssp). value = edges relaxed by all ranks / max-over-ranks
+persistent CTA of 4 warps (k_sssp_bank). value = edges relaxed by all ranks / max-over-ranks
 device time. The single-source (configs[2]) latency-bound number is reported
 in "single_source".
 
@@ -311,7 +311,7 @@ def run_pbh(args, D):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": (traffic_ps * S if traffic_ps else None),
-                         "kernel": "k_sssp_fast<1024,4> (one warp per source)",
+                         "kernel": "k_sssp_bank<4,8,4> (one 128-thread CTA per source)",
                          "alg_bytes_per_launch": alg_bytes_launch},
             "cpu_baseline": cpu,
             "e2e": {"value": edges_per_step_all / (e2e_max / 1e3), "unit": "edges/s",

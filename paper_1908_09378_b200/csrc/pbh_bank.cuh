@@ -37,6 +37,7 @@
 #pragma once
 
 #include "pbh_kernels.cuh"
+#include "pbh_grid.cuh"
 
 namespace pbh_dev {
 
@@ -56,6 +57,7 @@ struct BankL0 {
   u32 occ[B];    // per-thread occupancy masks (bit i = slot i*B + t)
   u64 spl_p;
   u32 spl_k, spl_inf, qn, pad;
+  u64 pushes;    // push_down count (drives the 4-to-1 resolve schedule)
 };
 
 // One warp's offer and counters for the per-pass exchange.
@@ -326,7 +328,7 @@ struct BankHeap {
     occm = 0;
     for (u32 j = tid; j < n; j += B) {
       const u32 k = K[j];
-      const u64 rb = __ldg(off + k), re = __ldg(off + k + 1);
+      const u64 rb = off ? __ldg(off + k) : 0, re = off ? __ldg(off + k + 1) : 0;
       L.lk[j] = k;
       L.lp[j] = P[j];
       L.lrb[j] = rb;
@@ -505,7 +507,8 @@ __global__ void __launch_bounds__(32 * NW, 1)
   const bool grow_ok = cap_last > (u64)2 * C0 + max_deg + kBankQ;
   u32 par = 0;                // exchange parity
   bool rescan_due = false;    // this thread's bank minimum is stale
-  bool evict_due = false;     // replicated: some bank lacks room for a pass
+  // replicated: some bank lacks room for a pass (also after a resume)
+  bool evict_due = Bk::any(__popc(occm) > (int)(KI - PE), hc.scr());
   bool nx = false;            // the next extraction is known (cur)
   BankOffer cur{};
   bool fail_bad = false, fail_ovf = false;
@@ -760,6 +763,328 @@ __global__ void __launch_bounds__(32 * NW, 1)
       my->status = sm.status;
       my->detail = sm.detail;
     }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Op-trace interpreter on the banked level 0: Engine::run_trace
+// (engine.cpp:207-226) with update / bulk_update / extract_min / delete
+// (bucket_heap.cpp:79-146). CTA 0 replays the ops; CTAs 1..G-1 are the grid
+// helpers of the deep merges (pbh_grid.cuh). A bulk batch is validated in one
+// pass (no mutation before every precondition holds, bucket_heap.cpp:127-136)
+// and applied in passes of B elements, one per thread, with the SSSP engine's
+// three outcomes: decrease in place, new level-0 slot, push buffer.
+// ---------------------------------------------------------------------------
+template <int NW, int KI, int VT>
+struct TraceBankSmem {
+  BankSmem<NW, KI, VT> b;  // first: bank_smem() aliases it
+  GridSmem<32 * NW> g;
+};
+
+template <int NW, int KI, int VT>
+__global__ void __launch_bounds__(32 * NW, 1)
+    k_trace_bank(pbh_heap_dev* g, pbh_trace_dev tr, u64 op_begin, u64 op_end, u32* out_v,
+                 u64* out_p, pbh_kstatus* ks, BankL0<32 * NW, KI>* save, u32 allow_internal,
+                 GridJob* gj, u32 grid_min) {
+  using BH = BankHeap<NW, KI, VT>;
+  using HC = typename BH::HC;
+  using Bk = Blk<BH::B>;
+  constexpr u32 B = BH::B;
+  constexpr u32 C0 = BH::C0;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  TraceBankSmem<NW, KI, VT>& T = *reinterpret_cast<TraceBankSmem<NW, KI, VT>*>(dyn);
+  if (blockIdx.x > 0) {  // helper CTA: deep merges of the leader's heap
+    grid_helper_loop<B>(gj, T.g, T.g.scr);
+    return;
+  }
+  BankSmem<NW, KI, VT>& S = T.b;
+  typename HC::Sm& sm = S.hs;
+  HC hc{sm};
+  hc.load(g, S.bk[0], S.bp[0], S.bk[1], S.bp[1], true);
+  hc.bk = g->g_bk;
+  hc.bp = g->g_bp;
+  hc.pk = g->g_pk;
+  hc.pp = g->g_pp;
+  hc.rm = g->g_rm;
+  hc.bo = nullptr;
+  if (gridDim.x > 1) {
+    hc.gj = gj;
+    hc.gsz = gridDim.x;
+    hc.gs = &T.g;
+    hc.gmin = grid_min;
+    grid_leader_init<B>(T.g);
+  }
+  const u32 tid = threadIdx.x;
+  BankL0<B, KI>& L = S.l0;
+  BH H(hc, S, g->idx, nullptr);
+  pbh_idx_entry* const idx = g->idx;
+  const u64 universe = g->universe;
+  const u32 dmax = sm.d;
+  const bool debug = sm.debug != 0;
+  // restore the level-0 image
+  {
+    const u32* src = reinterpret_cast<const u32*>(save);
+    u32* dst = reinterpret_cast<u32*>(&L);
+    for (u32 i = tid; i < sizeof(BankL0<B, KI>) / 4; i += B) dst[i] = src[i];
+  }
+  for (u32 i = tid; i < 2 * B; i += B) (&S.dirty[0][0])[i] = 0;
+  Bk::sync();
+  H.occm = L.occ[tid];
+  H.rescan();
+  H.qn = L.qn;
+  H.live = hc.s.live;
+  H.pushes = L.pushes;
+  H.after_cold();
+  Bk::sync();
+  u32 occm = H.occm;
+  bool lhas = H.lhas;
+  u64 lmin_p = H.lmin_p;
+  u32 lmin_k = H.lmin_k, lmin_s = H.lmin_s;
+  i64 live = H.live;
+  u32 qn = H.qn;
+  u64 deep_n = H.deep_n;
+#define BANK_TO_H()     \
+  H.occm = occm;        \
+  H.lhas = lhas;        \
+  H.lmin_p = lmin_p;    \
+  H.lmin_k = lmin_k;    \
+  H.lmin_s = lmin_s;    \
+  H.live = live;        \
+  H.qn = qn;            \
+  H.deep_n = deep_n;
+#define BANK_FROM_H()   \
+  occm = H.occm;        \
+  lhas = H.lhas;        \
+  lmin_p = H.lmin_p;    \
+  lmin_k = H.lmin_k;    \
+  lmin_s = H.lmin_s;    \
+  live = H.live;        \
+  qn = H.qn;            \
+  deep_n = H.deep_n;
+  const u32 Lnl = sm.n_levels;
+  const u64 cap_last = Lnl == 1 ? (u64)sm.cap0 : sm.lv[Lnl - 1].cap_b;
+  u32 par = 0;
+  bool rescan_due = false;
+  // a bank may be full already (the image of the previous launch)
+  bool evict_due = __syncthreads_or(__popc(occm) > KI - 1) != 0;
+  u64 n_out = ks->n_out;
+  u64 op = op_begin;
+  for (; op < op_end; ++op) {
+    const u8 kind = tr.kinds[op];
+    const u64 ob = tr.offsets[op], oe = tr.offsets[op + 1];
+    if (kind == 'U' || kind == 'B') {
+      // ------------------------------------------------ bulk_update / update
+      const u32* vals = tr.vals + ob;
+      const u64* prios = tr.prios + ob;
+      const u64 n64 = oe - ob;
+      const bool check = kind == 'B';
+      if (check && n64 == 0) {
+        hc.fail(PBH_ERR_EMPTY_BATCH);
+        break;
+      }
+      if (check && n64 > dmax) {
+        hc.fail(PBH_ERR_BATCH_TOO_BIG, n64);
+        break;
+      }
+      const u32 n = (u32)n64;
+      if ((u64)2 * C0 + qn + deep_n + n + kBankQ > cap_last) {
+        hc.fail(PBH_ERR_NEED_GROW, Lnl);
+        break;
+      }
+      // pass 1: validate (no mutation)
+      bool bad_sort = false, bad_key = false, bad_dead = false, bad_inc = false;
+      for (u32 j = tid; j < n; j += B) {
+        const u32 k = vals[j];
+        if (check && j > 0 && vals[j - 1] >= k) bad_sort = true;
+        if (k >= universe) {
+          bad_key = true;
+          continue;
+        }
+        const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + k));
+        if (PBH_ST((u32)e.y) == PBH_ST_DEAD) bad_dead = true;
+        if (debug && PBH_ST((u32)e.y) == PBH_ST_LIVE && prios[j] > e.x) bad_inc = true;
+      }
+      const u32 bad = (u32)__syncthreads_or(bad_sort) | ((u32)__syncthreads_or(bad_key) << 1) |
+                      ((u32)__syncthreads_or(bad_dead) << 2) | ((u32)__syncthreads_or(bad_inc) << 3);
+      if (bad) {
+        hc.fail(bad & 1 ? PBH_ERR_UNSORTED : bad & 2 ? PBH_ERR_KEY_RANGE
+                : bad & 4 ? PBH_ERR_REINSERT : PBH_ERR_INCREASE);
+        break;
+      }
+      // pass 2: apply, one element per thread per pass
+      bool cold_fail = false;
+      for (u32 base = 0; base < n; base += B) {
+        if (evict_due || qn > (u32)(kBankQ - B)) {
+          BANK_TO_H();
+          if (evict_due) H.evict();
+          if (!hc.failed() && H.qn > (u32)(kBankQ - B)) H.flush_q();
+          BANK_FROM_H();
+          if (evict_due) rescan_due = false;
+          evict_due = false;
+          if (hc.failed()) {
+            cold_fail = true;
+            break;
+          }
+        }
+        const u32 j = base + tid;
+        bool fresh = false, pushed = false;
+        if (j < n) {
+          const u32 u = vals[j];
+          const u64 c = prios[j];
+          const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + u));
+          const u32 st = (u32)e.y;
+          fresh = PBH_ST(st) != PBH_ST_LIVE;
+          if (fresh || c < e.x) {
+            const u32 loc = st >> 2;
+            u32 nst;
+            if (!fresh && loc < C0) {
+              L.lp[loc] = c;  // decrease in place; the owner rescans
+              S.dirty[par][loc % B] = 1;
+              nst = st;
+            } else if (L.spl_inf || c < L.spl_p || (c == L.spl_p && u <= L.spl_k)) {
+              const u32 i = __ffs(~occm) - 1;
+              const u32 sl = i * B + tid;
+              occm |= 1u << i;
+              L.lk[sl] = u;
+              L.lp[sl] = c;
+              if (!lhas || less_pk(c, u, lmin_p, lmin_k)) {
+                lhas = true;
+                lmin_p = c;
+                lmin_k = u;
+                lmin_s = sl;
+              }
+              nst = PBH_ST_LIVE | (sl << 2);
+            } else {
+              const u32 qp_ = atomicAdd(&L.qn, 1u);
+              L.qk[qp_] = u;
+              L.qp[qp_] = c;
+              pushed = true;
+              nst = PBH_ST_LIVE | (PBH_LOC_DEEP << 2);
+            }
+            pbh_idx_entry ne;
+            ne.prio = c;
+            ne.state = nst;
+            ne.parent = 0;
+            reinterpret_cast<ulonglong2*>(idx)[u] = *reinterpret_cast<const ulonglong2*>(&ne);
+          }
+        }
+        live += __syncthreads_count(fresh);
+        qn += __syncthreads_count(pushed);
+        evict_due = __syncthreads_or(__popc(occm) > KI - 1) != 0;
+        if (S.dirty[par][tid]) {
+          S.dirty[par][tid] = 0;
+          rescan_due = true;
+        }
+        par ^= 1;
+      }
+      if (cold_fail) break;
+      if (tid == 0) sm.touches[0] += 2ull * n;
+    } else if (kind == 'E' || (kind == kOpFind && allow_internal)) {
+      // ------------------------------------------------ extract_min / find_min
+      if (live <= 0) {
+        hc.fail(PBH_ERR_EMPTY_HEAP);
+        break;
+      }
+      BankOffer r{};
+      bool cold_fail = false;
+      for (int guard = 0; guard < 64; ++guard) {
+        if (rescan_due) bank_rescan<B, KI>(L, tid, occm, lhas, lmin_p, lmin_k, lmin_s);
+        rescan_due = false;
+        r = bank_exchange<NW, KI, VT>(par, lhas, lmin_p, lmin_k, lmin_s, 0, 0, 0, 0);
+        par ^= 1;
+        if (r.has) break;
+        BANK_TO_H();
+        H.refill();
+        BANK_FROM_H();
+        rescan_due = false;
+        evict_due = false;
+        if (hc.failed()) {
+          cold_fail = true;
+          break;
+        }
+      }
+      if (cold_fail) break;
+      if (!r.has) {
+        hc.fail(PBH_ERR_INVARIANT, 0xE0);
+        break;
+      }
+      if (tid == 0) {
+        out_v[n_out] = r.k;
+        out_p[n_out] = r.p;
+      }
+      ++n_out;
+      if (kind == 'E') {
+        if (r.slot % B == tid) {
+          occm &= ~(1u << (r.slot / B));
+          rescan_due = true;
+        }
+        if (tid == 0) idx[r.k].state = PBH_ST_DEAD;
+        --live;
+      }
+    } else if (kind == 'D') {
+      // ------------------------------------------------ delete_value
+      const u32 k = tr.vals[ob];
+      if (k < universe) {
+        const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + k));
+        const u32 st = (u32)e.y;
+        Bk::sync();  // every thread has read the entry before it changes
+        if (PBH_ST(st) == PBH_ST_LIVE) {
+          const u32 loc = st >> 2;
+          if (loc < C0 && loc % B == tid) {
+            occm &= ~(1u << (loc / B));
+            rescan_due = true;
+          }
+          --live;
+        }
+        if (tid == 0) idx[k].state = PBH_ST_DEAD;  // deeper copies are now stale
+        Bk::sync();
+      }
+    } else if (kind == kOpDrain && allow_internal) {
+      BANK_TO_H();
+      H.flush_q();
+      if (!hc.failed()) {
+        H.to_cold();
+        hc.drain();
+        H.after_cold();
+      }
+      BANK_FROM_H();
+      if (hc.failed()) break;
+    } else {
+      hc.fail(PBH_ERR_BAD_OP, kind);
+      break;
+    }
+    if (kind != kOpFind && kind != kOpDrain && tid == 0) {
+      sm.ops += 1;
+      sm.resolves[0] += 1;
+    }
+  }
+  if (gridDim.x > 1) grid_run<B>(gj, gridDim.x, 1, Run{}, Run{}, 0, Sink{}, 0, T.g, T.g.scr);
+  BANK_TO_H();
+#undef BANK_TO_H
+#undef BANK_FROM_H
+  // persist the level-0 image
+  Bk::sync();
+  L.occ[tid] = H.occm;
+  if (tid == 0) {
+    L.qn = H.qn;
+    L.pushes = H.pushes;
+  }
+  Bk::sync();
+  {
+    const u32* src = reinterpret_cast<const u32*>(&L);
+    u32* dst = reinterpret_cast<u32*>(save);
+    for (u32 i = tid; i < sizeof(BankL0<B, KI>) / 4; i += B) dst[i] = src[i];
+  }
+  H.to_cold();
+  hc.store();
+  if (tid == 0) {
+    ks->status = sm.status;
+    ks->detail = sm.detail;
+    ks->aux = sm.aux;
+    ks->ops_done = op - op_begin;
+    ks->n_out = n_out;
+    ks->failed_op = op;
   }
 }
 

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -60,9 +61,23 @@ size_t heap_smem_bytes_nt(int nt) {
   }
 }
 
+size_t grid_smem_bytes_nt(int nt) {
+  switch (nt) {
+    case 32: return sizeof(GridSmem<32>);
+    case 256: return sizeof(GridSmem<256>);
+    default: return sizeof(GridSmem<1024>);
+  }
+}
+
 SmLayout make_layout(int nt, u32 cap0, u32 bc, u32 d, bool sssp) {
   SmLayout L{};
   u32 off = a16(heap_smem_bytes_nt(nt));
+  if (!sssp) {
+    L.off_grid = off;
+    off += a16(grid_smem_bytes_nt(nt));
+    L.grid_min = kGridMin;
+    if (const char* e = getenv("PBH_GRID_MIN")) L.grid_min = std::max(2, atoi(e));
+  }
   const u32 base = off;
   L.off_b0k0 = off; off += a16((u64)cap0 * 4);
   L.off_b0k1 = off; off += a16((u64)cap0 * 4);
@@ -92,7 +107,8 @@ SmLayout make_layout(int nt, u32 cap0, u32 bc, u32 d, bool sssp) {
 
 int pick_nt(u64 d) {
   if (const char* e = getenv("PBH_NT")) return atoi(e);
-  if (d <= 32) return 32;
+  // deep-level merges dominate small batches: a 256-thread CTA beats a warp
+  // even at d = 1 (C4 prefill at d = 32: 95 -> 28 us per op)
   if (d <= 256) return 256;
   return 1024;
 }
@@ -106,25 +122,89 @@ u32 pick_cap0(u64 d) {
 }
 
 // ------------------------------------------------------------ kernel table
+// The trace interpreter: CTA 0 replays the ops; with gj, CTAs 1..G-1 are the
+// grid helpers of pbh_grid.cuh (cooperative launch = guaranteed co-residency,
+// one CTA per SM).
 template <int NT>
 cudaError_t launch_trace(const SmLayout& L, cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr,
-                         u64 b, u64 e, u32* ov, u64* op, pbh_kstatus* ks, u32 internal) {
+                         u64 b, u64 e, u32* ov, u64* op, pbh_kstatus* ks, u32 internal,
+                         GridJob* gj) {
   auto fn = k_trace<NT, VT>;
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
   if (err != cudaSuccess) return err;
-  fn<<<1, NT, L.total, st>>>(g, tr, b, e, ov, op, ks, L, internal);
+  int G = 1;
+  if (gj) {
+    static int grid_cache[3] = {0, 0, 0};
+    int& gc = grid_cache[NT == 32 ? 0 : NT == 256 ? 1 : 2];
+    if (gc == 0) {
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, L.total);
+      gc = std::max(1, sms * std::min(per_sm, 1));
+      if (const char* s = getenv("PBH_GRID")) gc = std::max(1, std::min(gc, atoi(s)));
+    }
+    G = gc;
+  }
+  if (G > 1) {
+    err = cudaMemsetAsync(gj, 0, sizeof(GridJob), st);
+    if (err != cudaSuccess) return err;
+    SmLayout Lc = L;
+    u32 internal_c = internal;
+    void* args[] = {&g, &tr, &b, &e, &ov, &op, &ks, &Lc, &internal_c, &gj};
+    err = cudaLaunchCooperativeKernel((const void*)fn, dim3(G), dim3(NT), args, L.total, st);
+  } else {
+    fn<<<1, NT, L.total, st>>>(g, tr, b, e, ov, op, ks, L, internal, gj);
+    err = cudaGetLastError();
+  }
   g_launches++;
-  return cudaGetLastError();
+  return err;
 }
 
 cudaError_t launch_trace_nt(int nt, const SmLayout& L, cudaStream_t st, pbh_heap_dev* g,
                             pbh_trace_dev tr, u64 b, u64 e, u32* ov, u64* op, pbh_kstatus* ks,
-                            u32 internal) {
+                            u32 internal, GridJob* gj) {
   switch (nt) {
-    case 32: return launch_trace<32>(L, st, g, tr, b, e, ov, op, ks, internal);
-    case 256: return launch_trace<256>(L, st, g, tr, b, e, ov, op, ks, internal);
-    default: return launch_trace<1024>(L, st, g, tr, b, e, ov, op, ks, internal);
+    case 32: return launch_trace<32>(L, st, g, tr, b, e, ov, op, ks, internal, gj);
+    case 256: return launch_trace<256>(L, st, g, tr, b, e, ov, op, ks, internal, gj);
+    default: return launch_trace<1024>(L, st, g, tr, b, e, ov, op, ks, internal, gj);
   }
+}
+
+// Banked op-trace interpreter (pbh_bank.cuh): 4 warps, level 0 = 1024 slots.
+constexpr int kTraceNW = 4;
+constexpr int kTraceKI = 8;
+using TraceImage = BankL0<32 * kTraceNW, kTraceKI>;
+using TraceSmem = TraceBankSmem<kTraceNW, kTraceKI, VT>;
+
+cudaError_t launch_trace_bank(cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr, u64 b, u64 e,
+                              u32* ov, u64* op, pbh_kstatus* ks, TraceImage* save, u32 internal,
+                              GridJob* gj, u32 grid_min) {
+  auto fn = k_trace_bank<kTraceNW, kTraceKI, VT>;
+  const int smem = (int)sizeof(TraceSmem);
+  static int G = 0;
+  if (G == 0) {
+    cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kTraceNW, smem);
+    G = std::max(1, sms * std::min(per_sm, 1));
+    if (const char* s = getenv("PBH_GRID")) G = std::max(1, std::min(G, atoi(s)));
+  }
+  cudaError_t err;
+  if (gj && G > 1) {
+    err = cudaMemsetAsync(gj, 0, sizeof(GridJob), st);
+    if (err != cudaSuccess) return err;
+    void* args[] = {&g, &tr, &b, &e, &ov, &op, &ks, &save, &internal, &gj, &grid_min};
+    err = cudaLaunchCooperativeKernel((const void*)fn, dim3(G), dim3(32 * kTraceNW), args, smem, st);
+  } else {
+    fn<<<1, 32 * kTraceNW, smem, st>>>(g, tr, b, e, ov, op, ks, save, internal, gj, grid_min);
+    err = cudaGetLastError();
+  }
+  g_launches++;
+  return err;
 }
 
 template <int NT>
@@ -400,6 +480,10 @@ struct pbh_heap {
   SmLayout layout{};
   pbh_kstatus* d_ks = nullptr;
   pbh_kstatus* h_ks = nullptr;  // pinned
+  GridJob* d_job = nullptr;     // grid-helper job word (null: single-CTA engine)
+  bool bank = true;             // banked level-0 interpreter (false: sorted-B_0 CTA engine)
+  TraceImage* d_save = nullptr; // its level-0 image between launches
+  u32 grid_min = kGridMin;
   // staging for host traces
   u64 st_ops = 0, st_el = 0, st_out = 0;
   u8* d_kinds = nullptr;
@@ -443,7 +527,7 @@ pbh_status ensure_staging(pbh_heap* h, u64 n_ops, u64 n_el, u64 n_out) {
 
 // Make sure the batch scratch can hold batches of up to n elements.
 pbh_status ensure_batch(pbh_heap* h, u64 n) {
-  if (n <= h->H.bc) return PBH_OK;
+  if (h->bank || n <= h->H.bc) return PBH_OK;  // the banked engine needs no batch scratch
   u32 bc = (u32)pow2_at_least(n);
   DevHeap& H = h->H;
   CK(cudaMemcpyAsync(&H.hd, H.dev, sizeof(pbh_heap_dev), cudaMemcpyDeviceToHost, h->stream));
@@ -471,8 +555,13 @@ pbh_status exec_trace(pbh_heap* h, u64 n_ops, pbh_trace_dev tr, u32* d_ov, u64* 
   for (int guard = 0; guard < 4096; ++guard) {
     if (begin >= n_ops) break;
     CK(cudaEventRecord(h->ev0, h->stream));
-    CK(launch_trace_nt(h->nt, h->layout, h->stream, h->H.dev, tr, begin, n_ops, d_ov, d_op,
-                       h->d_ks, internal));
+    if (h->bank) {
+      CK(launch_trace_bank(h->stream, h->H.dev, tr, begin, n_ops, d_ov, d_op, h->d_ks, h->d_save,
+                           internal, h->d_job, h->grid_min));
+    } else {
+      CK(launch_trace_nt(h->nt, h->layout, h->stream, h->H.dev, tr, begin, n_ops, d_ov, d_op,
+                         h->d_ks, internal, h->d_job));
+    }
     CK(cudaEventRecord(h->ev1, h->stream));
     CK(cudaMemcpyAsync(h->h_ks, h->d_ks, sizeof(pbh_kstatus), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -589,8 +678,10 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
   h->device = device;
   h->d = d;
   h->nt = pick_nt(d);
+  if (const char* e = getenv("PBH_TRACE_ENGINE")) h->bank = std::string(e) != "cta";
+  if (h->bank) h->nt = 32 * kTraceNW;
   if (key_universe == 0) key_universe = 1 << 16;
-  const u32 cap0 = pick_cap0(d);
+  const u32 cap0 = h->bank ? (u32)(32 * kTraceNW * kTraceKI / 2) : pick_cap0(d);
   const u32 bc = (u32)pow2_at_least(std::max<u64>(std::min<u64>(d, 4096), 2));
   auto fail = [&](pbh_status s) {
     h->H.free_all();
@@ -605,6 +696,21 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
   if (cudaMalloc(&h->d_ks, sizeof(pbh_kstatus)) != cudaSuccess ||
       cudaMallocHost(&h->h_ks, sizeof(pbh_kstatus)) != cudaSuccess)
     return fail(set_err(PBH_OOM, "status block allocation failed"));
+  // grid helpers for the deep merges (PBH_GRID=1 disables them)
+  const char* ge = getenv("PBH_GRID");
+  if (!(ge && atoi(ge) <= 1) && cudaMalloc(&h->d_job, sizeof(GridJob)) != cudaSuccess)
+    return fail(set_err(PBH_OOM, "grid job allocation failed"));
+  if (h->bank) {
+    if (cudaMalloc(&h->d_save, sizeof(TraceImage)) != cudaSuccess)
+      return fail(set_err(PBH_OOM, "level-0 image allocation failed"));
+    TraceImage* img = new TraceImage();
+    std::memset(img, 0, sizeof(TraceImage));
+    img->spl_inf = 1;
+    cudaError_t e = cudaMemcpy(h->d_save, img, sizeof(TraceImage), cudaMemcpyHostToDevice);
+    delete img;
+    if (e != cudaSuccess) return fail(set_err(PBH_CUDA, "level-0 image init failed"));
+  }
+  if (const char* e = getenv("PBH_GRID_MIN")) h->grid_min = std::max(2, atoi(e));
   cudaEventCreate(&h->ev0);
   cudaEventCreate(&h->ev1);
   *out = h;
@@ -618,6 +724,8 @@ pbh_status pbh_heap_destroy(pbh_heap* h) {
   h->H.free_all();
   cudaFree(h->d_ks);
   cudaFreeHost(h->h_ks);
+  cudaFree(h->d_job);
+  cudaFree(h->d_save);
   cudaFree(h->d_kinds);
   cudaFree(h->d_off);
   cudaFree(h->d_vals);
@@ -737,6 +845,42 @@ pbh_status pbh_heap_check_invariants(pbh_heap* h, uint64_t* n_violations) {
   bool have_prev = false;
   u64 prev_p = 0;
   u32 prev_k = 0;  // max of all buckets so far
+  auto valid0 = [&](u32 k, u64 p) {
+    return k < hd.universe && PBH_ST(idx[k].state) == PBH_ST_LIVE && idx[k].prio == p;
+  };
+  if (h->bank) {
+    // banked level 0 (pbh_bank.cuh): every occupied slot holds a valid entry
+    // whose index records that slot, all admitted by splitter_0; the push
+    // buffer holds entries beyond it
+    std::unique_ptr<TraceImage> img(new TraceImage());
+    CK(cudaMemcpy(img.get(), h->d_save, sizeof(TraceImage), cudaMemcpyDeviceToHost));
+    constexpr u32 Bn = 32 * kTraceNW;
+    for (u32 t = 0; t < Bn; ++t)
+      for (u32 i = 0; i < (u32)kTraceKI; ++i) {
+        if (!((img->occ[t] >> i) & 1u)) continue;
+        const u32 sl = i * Bn + t;
+        const u32 k = img->lk[sl];
+        const u64 p = img->lp[sl];
+        if (!valid0(k, p)) complain("level 0: stale entry in slot " + std::to_string(sl));
+        else if ((idx[k].state >> 2) != sl) complain("level 0: index does not record slot " + std::to_string(sl));
+        else ++valid_entries;
+        if (!(img->spl_inf || p < img->spl_p || (p == img->spl_p && k <= img->spl_k)))
+          complain("level 0: slot above splitter_0");
+      }
+    for (u32 j = 0; j < img->qn; ++j) {
+      const u32 k = img->qk[j];
+      const u64 p = img->qp[j];
+      if (!valid0(k, p)) continue;
+      ++valid_entries;
+      if (img->spl_inf || p < img->spl_p || (p == img->spl_p && k <= img->spl_k))
+        complain("level 0: push-buffer entry admitted by splitter_0");
+    }
+    if (!img->spl_inf) {
+      have_prev = true;
+      prev_p = img->spl_p;
+      prev_k = img->spl_k;
+    }
+  }
   for (u32 i = 0; i < hd.n_levels; ++i) {
     const pbh_level_state& t = hd.st[i];
     const pbh_level_bufs& b = hd.lv[i];

@@ -4,7 +4,7 @@
 // state lives in shared memory and is written by thread 0 between barriers.
 #pragma once
 
-#include "pbh_engine.cuh"
+#include "pbh_grid.cuh"
 
 namespace pbh_dev {
 
@@ -46,6 +46,32 @@ struct HeapCta {
   u32* b0k_global[2];
   u64* b0p_global[2];
   bool b0_in_smem;
+  // grid helpers for deep merges (trace interpreter only; null = CTA-local)
+  GridJob* gj = nullptr;
+  u32 gsz = 1;
+  u32 gmin = kGridMin;  // smallest merge sent to the grid
+  GridSmem<NT>* gs = nullptr;
+
+  // Merge / copy dispatch: a big merge runs on the whole grid (unfiltered,
+  // see pbh_grid.cuh), anything else in this CTA with the index filter.
+  // helpers cannot see this CTA's shared memory: grid jobs take HBM runs only
+  DEV static bool hbm(const void* p) { return p == nullptr || !__isShared(p); }
+  DEV static bool hbm_sink(const Sink& k) { return hbm(k.k1) && (k.lim == kInfCount || hbm(k.k2)); }
+  NOINL u32 mrg(const Run& A, const Run& B, bool filter, const Sink& snk, u32 out_base) {
+    const u32 tot = A.n + B.n;
+    if (gj && tot >= gmin && hbm(A.k) && hbm(B.k) && hbm_sink(snk)) {
+      grid_run<NT>(gj, gsz, 0, A, B, tot, snk, out_base, *gs, gs->scr);
+      return tot;
+    }
+    return merge_runs<NT, VT>(A, B, filter, idx, snk, out_base, s.tile, scr());
+  }
+  NOINL u32 cpy(const Run& A, bool filter, const Sink& snk, u32 out_base) {
+    if (gj && A.n >= gmin && hbm(A.k) && hbm_sink(snk)) {
+      grid_run<NT>(gj, gsz, 0, A, Run{A.k, A.p, 0}, A.n, snk, out_base, *gs, gs->scr);
+      return A.n;
+    }
+    return copy_run<NT, VT>(A, filter, idx, snk, out_base, scr());
+  }
 
   DEV bool t0() const { return threadIdx.x == 0; }
   DEV u32* scr() { return s.scratch; }
@@ -182,7 +208,7 @@ struct HeapCta {
     const Run Sj = signal(j);
     const u32 ns = 1 - s.st[j].s_sel;
     const Sink snk{s.lv[j].sk[ns], s.lv[j].sp[ns], kInfCount, nullptr, nullptr};
-    const u32 n = merge_runs<NT, VT>(Sj, X, true, idx, snk, 0, s.tile, scr());
+    const u32 n = mrg(Sj, X, true, snk, 0);
     if (t0()) {
       s.st[j].s_sel = ns;
       s.st[j].s_head = 0;
@@ -207,11 +233,11 @@ struct HeapCta {
     const pbh_level_bufs& L = s.lv[i];
     const u32 nb = 1 - s.st[i].b_sel, ns = 1 - s.st[i].s_sel;
     const Sink snk{L.bk[nb], L.bp[nb], L.cap_b, L.sk[ns], L.sp[ns]};
-    const u32 n = merge_runs<NT, VT>(Br, Sa, true, idx, snk, 0, s.tile, scr());
+    const u32 n = mrg(Br, Sa, true, snk, 0);
     const u32 keep = n < L.cap_b ? n : L.cap_b;
     const u32 over = n - keep;
     const Sink snk2{L.sk[ns], L.sp[ns], kInfCount, nullptr, nullptr};
-    const u32 nr = copy_run<NT, VT>(Sb, true, idx, snk2, over, scr());
+    const u32 nr = cpy(Sb, true, snk2, over);
     if (t0()) {
       pbh_level_state& t = s.st[i];
       t.b_sel = nb;
@@ -257,7 +283,7 @@ struct HeapCta {
     const Run Bi = bucket(i);
     const u32 nb = 1 - s.st[i].b_sel;
     const Sink dst{L.bk[nb], L.bp[nb], kInfCount, nullptr, nullptr};
-    u32 n = copy_run<NT, VT>(Bi, i > 0, idx, dst, 0, scr());
+    u32 n = cpy(Bi, i > 0, dst, 0);
     const Run Bj = bucket(j);
     const Run Sj = signal(j);
     const u32 adm = count_admitted<NT>(Sj, s.st[j], scr());
@@ -268,9 +294,12 @@ struct HeapCta {
       const u32 need = cap - n;
       const u32 avail = (Bj.n - ha) + (adm - hb);
       u32 c = need < avail ? need : avail;
-      if (c > T) c = T;
+      // deep refills pull a whole prefix on the grid (unfiltered); level 0
+      // is always refilled here, tile by tile, through the index filter
       const Run A{Bj.k + ha, Bj.p + ha, Bj.n - ha};
       const Run B{Sj.k + hb, Sj.p + hb, adm - hb};
+      const bool on_grid = gj && i > 0 && c >= gmin && hbm(A.k) && hbm(B.k) && hbm_sink(dst);
+      if (!on_grid && c > T) c = T;
       const u32 a = merge_split<NT>(A, B, c, scr());
       // last element of the tile in merged order
       {
@@ -285,7 +314,12 @@ struct HeapCta {
           last_k = kb;
         }
       }
-      n += merge_tile<NT, VT>(A, 0, a, B, 0, c - a, true, idx, dst, n, s.tile, scr());
+      if (on_grid) {
+        grid_run<NT>(gj, gsz, 0, A, B, c, dst, n, *gs, gs->scr);
+        n += c;
+      } else {
+        n += merge_tile<NT, VT>(A, 0, a, B, 0, c - a, true, idx, dst, n, s.tile, scr());
+      }
       ha += a;
       hb += c - a;
     }
@@ -427,11 +461,11 @@ struct HeapCta {
     const Run B0 = bucket(0);
     const u32 nb = 1 - s.st[0].b_sel;
     const Sink snk{s.lv[0].bk[nb], s.lv[0].bp[nb], s.cap0, pk, pp};
-    const u32 tot = merge_runs<NT, VT>(B0, Na, false, idx, snk, 0, s.tile, scr());
+    const u32 tot = mrg(B0, Na, false, snk, 0);
     const u32 keep = tot < s.cap0 ? tot : s.cap0;
     const u32 over = tot - keep;
     const Sink snk2{pk, pp, kInfCount, nullptr, nullptr};
-    const u32 nr = copy_run<NT, VT>(Nb, false, idx, snk2, over, scr());
+    const u32 nr = cpy(Nb, false, snk2, over);
     if (t0()) {
       pbh_level_state& t = s.st[0];
       t.b_sel = nb;

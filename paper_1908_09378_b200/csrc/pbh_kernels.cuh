@@ -10,6 +10,8 @@ namespace pbh_dev {
 // Dynamic shared-memory layout (byte offsets), computed on the host.
 struct SmLayout {
   u32 use_smem;  // B_0 + batch + push + removal flags resident in smem
+  u32 off_grid;  // GridSmem<NT> (trace interpreter with grid helpers)
+  u32 grid_min;  // smallest merge sent to the grid helpers
   u32 off_b0k0, off_b0k1, off_b0p0, off_b0p1;
   u32 off_bk, off_bp, off_pk, off_pp, off_rm;
   u32 off_ck, off_cp, off_co, off_cs;  // SSSP relaxation collection (d + NT)
@@ -56,12 +58,25 @@ DEV void bind_buffers(HeapCta<NT, VT>& h, unsigned char* dyn, const SmLayout& L,
 template <int NT, int VT>
 __global__ void __launch_bounds__(NT) k_trace(pbh_heap_dev* g, pbh_trace_dev tr, u64 op_begin,
                                               u64 op_end, u32* out_v, u64* out_p,
-                                              pbh_kstatus* ks, SmLayout L, u32 allow_internal) {
+                                              pbh_kstatus* ks, SmLayout L, u32 allow_internal,
+                                              GridJob* gj) {
   extern __shared__ __align__(16) unsigned char dyn[];
   using HC = HeapCta<NT, VT>;
   using Bk = Blk<NT>;
+  GridSmem<NT>& gsm = *reinterpret_cast<GridSmem<NT>*>(dyn + L.off_grid);
+  if (blockIdx.x > 0) {  // helper CTA: deep merges of the leader's heap
+    grid_helper_loop<NT>(gj, gsm, gsm.scr);
+    return;
+  }
   typename HC::Sm& sm = *reinterpret_cast<typename HC::Sm*>(dyn);
   HC h{sm};
+  if (gridDim.x > 1) {
+    h.gj = gj;
+    h.gsz = gridDim.x;
+    h.gs = &gsm;
+    h.gmin = L.grid_min;
+    grid_leader_init<NT>(gsm);
+  }
   h.load(g, reinterpret_cast<u32*>(dyn + L.off_b0k0), reinterpret_cast<u64*>(dyn + L.off_b0p0),
          reinterpret_cast<u32*>(dyn + L.off_b0k1), reinterpret_cast<u64*>(dyn + L.off_b0p1),
          L.use_smem != 0);
@@ -127,6 +142,7 @@ __global__ void __launch_bounds__(NT) k_trace(pbh_heap_dev* g, pbh_trace_dev tr,
       break;
     }
   }
+  if (gridDim.x > 1) grid_run<NT>(gj, gridDim.x, 1, Run{}, Run{}, 0, Sink{}, 0, gsm, gsm.scr);
   h.store();
   if (threadIdx.x == 0) {
     ks->status = sm.status;

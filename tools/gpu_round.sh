@@ -1,4 +1,3 @@
 set -x
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1
-tail -n 4 gpurun_out/pytest_gpu.log gpurun_out/bench.log
+for gm in 256 1024 4096 16384; do PBH_GRID_MIN=$gm timeout 600 python tools/probe_trace.py c1 fill > gpurun_out/trace_gm$gm.log 2>&1; done
+tail -n 5 gpurun_out/trace_gm*.log | cut -c1-200

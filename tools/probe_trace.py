@@ -22,9 +22,9 @@ def run(name, tr, d, universe):
 which = sys.argv[1:] or ["c1", "fill"]
 if "c1" in which:
     run("c1_20k", gen.mixed_trace(20000, 1 << 20, 1024, 1), 1024, 1 << 20)
-if "fill" in which:
-    for d in (32, 1024):
-        n = 1 << 20
+if "fill" in which or "fill32" in which:
+    for d in ((32,) if "fill32" in which else (32, 1024)):
+        n = 1 << (16 if "fill32" in which else 20)
         pr = gen.sweep_prefill(n, 4)
 
         class T:
