@@ -41,7 +41,7 @@
 
 namespace pbh_dev {
 
-constexpr int kBankQ = 512;     // push-buffer capacity (entries beyond the splitter)
+constexpr int kBankQ = 4096;    // push-buffer capacity (entries beyond the splitter)
 constexpr int kBankPass = 256;  // edges relaxed per pass
 
 // The part of the shared-memory image that survives a NEED_GROW relaunch.
@@ -76,6 +76,8 @@ struct BankSmem {
   // it is also the sort scratch of evict()
   u32 bk[2][C0 / 2];
   u64 bp[2][C0 / 2];
+  u32 sk[kBankQ];  // sort scratch of the push-buffer flush
+  u64 sp[kBankQ];
   u32 pf_t[kBankPass];  // next row's first pass, prefetched by cp.async
   u32 pf_w[kBankPass];
   BankOffer ex[2][NW];  // per-pass exchange (parity double-buffered)
@@ -88,24 +90,6 @@ DEV BankSmem<NW, KI, VT>& bank_smem() {
   extern __shared__ __align__(16) unsigned char dyn[];
   return *reinterpret_cast<BankSmem<NW, KI, VT>*>(dyn);
 }
-
-// 4-byte global -> shared copy that bypasses registers (zero-fill when !pred).
-DEV void cp_async4(void* smem, const void* gmem, bool pred) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem),
-               "r"(pred ? 4 : 0)
-               : "memory");
-}
-// Bulk L2 prefetch of the 4-byte array range [a[i0], a[i1]) (16-byte granular).
-DEV void l2_prefetch_range(const u32* a, u64 i0, u64 i1) {
-  const u64 b0 = (reinterpret_cast<u64>(a + i0)) & ~15ull;
-  const u64 b1 = (reinterpret_cast<u64>(a + i1) + 15) & ~15ull;
-  if (b1 > b0)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(b0), "r"((u32)(b1 - b0))
-                 : "memory");
-}
-DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // warp argmin of (p, k) over lanes with `has`; returns the winning lane.
 DEV u32 warp_argmin(bool& has, u64& p, u32& k) {
@@ -227,6 +211,125 @@ DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u
   }
 }
 
+// Sort n <= kBankQ entries (K, P) in shared memory by (p, k) with the whole
+// CTA: the warps sort runs of 128 in registers (4 per lane, element
+// r*32 + lane; bitonic network, shuffles below stride 32), then merge-path
+// rounds (4 outputs per thread per step) double the run width, ping-ponging
+// through (TK, TP). Slots n.. of the padded width are (~0, ~0): they sort last.
+template <int NW>
+DEV void cta_sort(u32* K, u64* P, u32 n, u32* TK, u64* TP) {
+  constexpr u32 NT = 32 * NW;
+  const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  u32 M = 128;
+  while (M < n) M <<= 1;
+  for (u32 run = w; run * 128 < M; run += NW) {
+    u64 p[4];
+    u32 k[4];
+#pragma unroll
+    for (u32 r = 0; r < 4; ++r) {
+      const u32 i = run * 128 + r * 32 + lane;
+      p[r] = i < n ? P[i] : ~0ull;
+      k[r] = i < n ? K[i] : 0xffffffffu;
+    }
+#pragma unroll
+    for (u32 size = 2; size <= 128; size <<= 1) {
+#pragma unroll
+      for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
+        if (stride >= 32) {
+          const u32 rs = stride / 32;
+#pragma unroll
+          for (u32 r = 0; r < 4; ++r) {
+            if (r & rs) continue;
+            const u32 i = r * 32 + lane;  // lower element of the pair
+            const bool up = (i & size) == 0;
+            const bool gt = less_pk(p[r | rs], k[r | rs], p[r], k[r]);
+            if (gt == up) {
+              const u64 tp = p[r];
+              p[r] = p[r | rs];
+              p[r | rs] = tp;
+              const u32 tk = k[r];
+              k[r] = k[r | rs];
+              k[r | rs] = tk;
+            }
+          }
+        } else {
+#pragma unroll
+          for (u32 r = 0; r < 4; ++r) {
+            const u32 i = r * 32 + lane;
+            const u32 ohi = __shfl_xor_sync(0xffffffffu, (u32)(p[r] >> 32), stride);
+            const u32 olo = __shfl_xor_sync(0xffffffffu, (u32)p[r], stride);
+            const u32 ok = __shfl_xor_sync(0xffffffffu, k[r], stride);
+            const u64 op = ((u64)ohi << 32) | olo;
+            const bool up = (i & size) == 0;
+            const bool lower = (lane & stride) == 0;
+            const bool other_less = less_pk(op, ok, p[r], k[r]);
+            if (lower == up ? other_less : !other_less) {
+              p[r] = op;
+              k[r] = ok;
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (u32 r = 0; r < 4; ++r) {
+      K[run * 128 + r * 32 + lane] = k[r];
+      P[run * 128 + r * 32 + lane] = p[r];
+    }
+  }
+  __syncthreads();
+  u32* sk = K;
+  u64* sp = P;
+  u32* dk = TK;
+  u64* dp = TP;
+  for (u32 wr = 128; wr < M; wr <<= 1) {
+    for (u32 o0 = tid * 4; o0 < M; o0 += 4 * NT) {
+      const u32 base = (o0 / (2 * wr)) * 2 * wr;
+      const u32 d = o0 - base;
+      const u32* ak = sk + base;
+      const u64* ap = sp + base;
+      const u32* bk = sk + base + wr;
+      const u64* bp = sp + base + wr;
+      u32 lo = d > wr ? d - wr : 0, hi = d < wr ? d : wr;
+      while (lo < hi) {
+        const u32 m = (lo + hi) >> 1;
+        if (less_pk(ap[m], ak[m], bp[d - 1 - m], bk[d - 1 - m]))
+          lo = m + 1;
+        else
+          hi = m;
+      }
+      u32 x = lo, y = d - lo;
+#pragma unroll
+      for (u32 v = 0; v < 4; ++v) {
+        const bool ta = x < wr && (y >= wr || less_pk(ap[x], ak[x], bp[y], bk[y]));
+        if (ta) {
+          dk[o0 + v] = ak[x];
+          dp[o0 + v] = ap[x];
+          ++x;
+        } else {
+          dk[o0 + v] = bk[y];
+          dp[o0 + v] = bp[y];
+          ++y;
+        }
+      }
+    }
+    __syncthreads();
+    u32* t1 = sk;
+    sk = dk;
+    dk = t1;
+    u64* t2 = sp;
+    sp = dp;
+    dp = t2;
+  }
+  if (sk != K) {
+    for (u32 i = tid; i < n; i += NT) {
+      K[i] = sk[i];
+      P[i] = sp[i];
+    }
+    __syncthreads();
+  }
+}
+
 template <int NW, int KI, int VT>
 struct BankHeap {
   static constexpr int B = 32 * NW;
@@ -254,6 +357,14 @@ struct BankHeap {
   u64 deep_n;
   u32 n_l0;
   u32 qn;  // push-buffer fill (mirrors L.qn at pass boundaries)
+  unsigned long long* prof = nullptr;  // PBH_PROF counters 8.. (cold-path breakdown)
+  DEV void pr(int i, long long& t) {
+    if (prof && tid == 0) {
+      const long long t1 = clock64();
+      atomicAdd(prof + i, (unsigned long long)(t1 - t));
+      t = t1;
+    }
+  }
 
   DEV BankHeap(HC& h, SM& s, pbh_idx_entry* ix, const u64* of)
       : hc(h), S(s), L(s.l0), idx(ix), off(of), tid(threadIdx.x) {}
@@ -300,12 +411,15 @@ struct BankHeap {
   // Merge the sorted run (K, P)[0, n) into S_1 and run the 4-to-1 schedule.
   NOINL void push_run(const u32* K, const u64* P, u32 n) {
     if (n == 0) return;
+    long long t = clock64();
     to_cold();
     hc.template push_down<true>(0, Run{K, P, n});
+    pr(9, t);
     ++pushes;
     for (u32 i = 1; i < hc.s.n_levels && i < 31 && !hc.failed(); ++i) {
       if (pushes & ((1ull << (2 * i)) - 1)) break;  // resolve(i) every 4^i pushes
       hc.resolve(i);
+      pr(9 + (i < 6 ? i : 6), t);
     }
     after_cold();
   }
@@ -314,7 +428,9 @@ struct BankHeap {
     Bk::sync();
     const u32 n = qn;
     if (n == 0) return;
-    bitonic_sort<B>(L.qk, L.qp, n);
+    long long t = clock64();
+    cta_sort<NW>(L.qk, L.qp, n, S.sk, S.sp);
+    pr(8, t);
     push_run(L.qk, L.qp, n);
     if (tid == 0) L.qn = 0;
     qn = 0;
@@ -786,7 +902,7 @@ template <int NW, int KI, int VT>
 __global__ void __launch_bounds__(32 * NW, 1)
     k_trace_bank(pbh_heap_dev* g, pbh_trace_dev tr, u64 op_begin, u64 op_end, u32* out_v,
                  u64* out_p, pbh_kstatus* ks, BankL0<32 * NW, KI>* save, u32 allow_internal,
-                 GridJob* gj, u32 grid_min) {
+                 GridJob* gj, u32 grid_min, unsigned long long* prof) {
   using BH = BankHeap<NW, KI, VT>;
   using HC = typename BH::HC;
   using Bk = Blk<BH::B>;
@@ -808,16 +924,17 @@ __global__ void __launch_bounds__(32 * NW, 1)
   hc.pp = g->g_pp;
   hc.rm = g->g_rm;
   hc.bo = nullptr;
+  hc.gs = &T.g;  // streamed CTA-local merges
   if (gridDim.x > 1) {
     hc.gj = gj;
     hc.gsz = gridDim.x;
-    hc.gs = &T.g;
     hc.gmin = grid_min;
     grid_leader_init<B>(T.g);
   }
   const u32 tid = threadIdx.x;
   BankL0<B, KI>& L = S.l0;
   BH H(hc, S, g->idx, nullptr);
+  H.prof = prof;
   pbh_idx_entry* const idx = g->idx;
   const u64 universe = g->universe;
   const u32 dmax = sm.d;
@@ -870,6 +987,15 @@ __global__ void __launch_bounds__(32 * NW, 1)
   bool evict_due = __syncthreads_or(__popc(occm) > KI - 1) != 0;
   u64 n_out = ks->n_out;
   u64 op = op_begin;
+  // PBH_PROF: leader-side cycle breakdown (thread 0), categories below
+  long long pt0 = clock64();
+  u64 pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define TPROF(i)                          \
+  if (prof) {                             \
+    const long long t1_ = clock64();      \
+    pc[i] += (u64)(t1_ - pt0);            \
+    pt0 = t1_;                            \
+  }
   for (; op < op_end; ++op) {
     const u8 kind = tr.kinds[op];
     const u64 ob = tr.offsets[op], oe = tr.offsets[op + 1];
@@ -905,6 +1031,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
         if (PBH_ST((u32)e.y) == PBH_ST_DEAD) bad_dead = true;
         if (debug && PBH_ST((u32)e.y) == PBH_ST_LIVE && prios[j] > e.x) bad_inc = true;
       }
+      TPROF(6);
       const u32 bad = (u32)__syncthreads_or(bad_sort) | ((u32)__syncthreads_or(bad_key) << 1) |
                       ((u32)__syncthreads_or(bad_dead) << 2) | ((u32)__syncthreads_or(bad_inc) << 3);
       if (bad) {
@@ -913,15 +1040,18 @@ __global__ void __launch_bounds__(32 * NW, 1)
         break;
       }
       // pass 2: apply, one element per thread per pass
+      TPROF(0);
       bool cold_fail = false;
       for (u32 base = 0; base < n; base += B) {
         if (evict_due || qn > (u32)(kBankQ - B)) {
+          TPROF(1);
           BANK_TO_H();
           if (evict_due) H.evict();
           if (!hc.failed() && H.qn > (u32)(kBankQ - B)) H.flush_q();
           BANK_FROM_H();
           if (evict_due) rescan_due = false;
           evict_due = false;
+          TPROF(2);
           if (hc.failed()) {
             cold_fail = true;
             break;
@@ -980,6 +1110,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
       }
       if (cold_fail) break;
       if (tid == 0) sm.touches[0] += 2ull * n;
+      TPROF(1);
     } else if (kind == 'E' || (kind == kOpFind && allow_internal)) {
       // ------------------------------------------------ extract_min / find_min
       if (live <= 0) {
@@ -994,9 +1125,11 @@ __global__ void __launch_bounds__(32 * NW, 1)
         r = bank_exchange<NW, KI, VT>(par, lhas, lmin_p, lmin_k, lmin_s, 0, 0, 0, 0);
         par ^= 1;
         if (r.has) break;
+        TPROF(3);
         BANK_TO_H();
         H.refill();
         BANK_FROM_H();
+        TPROF(4);
         rescan_due = false;
         evict_due = false;
         if (hc.failed()) {
@@ -1022,6 +1155,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
         if (tid == 0) idx[r.k].state = PBH_ST_DEAD;
         --live;
       }
+      TPROF(3);
     } else if (kind == 'D') {
       // ------------------------------------------------ delete_value
       const u32 k = tr.vals[ob];
@@ -1059,6 +1193,10 @@ __global__ void __launch_bounds__(32 * NW, 1)
       sm.resolves[0] += 1;
     }
   }
+  TPROF(5);
+#undef TPROF
+  if (prof && tid == 0)
+    for (int i = 0; i < 8; ++i) atomicAdd(prof + i, (unsigned long long)pc[i]);
   if (gridDim.x > 1) grid_run<B>(gj, gridDim.x, 1, Run{}, Run{}, 0, Sink{}, 0, T.g, T.g.scr);
   BANK_TO_H();
 #undef BANK_TO_H

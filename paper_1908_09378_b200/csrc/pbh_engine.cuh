@@ -55,6 +55,29 @@ DEV bool entry_valid(const pbh_idx_entry* idx, u32 k, u64 p) {
   return PBH_ST((u32)e.y) == PBH_ST_LIVE && e.x == p;
 }
 
+// 4-byte global -> shared copy that bypasses registers (zero-fill when !pred).
+DEV void cp_async4(void* smem, const void* gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(pred ? 4 : 0)
+               : "memory");
+}
+// Bulk L2 prefetch of the 4-byte array range [a[i0], a[i1]) (16-byte granular).
+DEV void l2_prefetch_range(const u32* a, u64 i0, u64 i1) {
+  const u64 b0 = (reinterpret_cast<u64>(a + i0)) & ~15ull;
+  const u64 b1 = (reinterpret_cast<u64>(a + i1) + 15) & ~15ull;
+  if (b1 > b0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(b0), "r"((u32)(b1 - b0))
+                 : "memory");
+}
+// 8-byte global -> shared copy (both 8-byte aligned).
+DEV void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // --------------------------------------------------------------------------
 // CTA primitives
 // --------------------------------------------------------------------------

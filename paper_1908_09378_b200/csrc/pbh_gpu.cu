@@ -179,7 +179,7 @@ using TraceSmem = TraceBankSmem<kTraceNW, kTraceKI, VT>;
 
 cudaError_t launch_trace_bank(cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr, u64 b, u64 e,
                               u32* ov, u64* op, pbh_kstatus* ks, TraceImage* save, u32 internal,
-                              GridJob* gj, u32 grid_min) {
+                              GridJob* gj, u32 grid_min, unsigned long long* prof) {
   auto fn = k_trace_bank<kTraceNW, kTraceKI, VT>;
   const int smem = (int)sizeof(TraceSmem);
   static int G = 0;
@@ -197,10 +197,11 @@ cudaError_t launch_trace_bank(cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr
   if (gj && G > 1) {
     err = cudaMemsetAsync(gj, 0, sizeof(GridJob), st);
     if (err != cudaSuccess) return err;
-    void* args[] = {&g, &tr, &b, &e, &ov, &op, &ks, &save, &internal, &gj, &grid_min};
+    void* args[] = {&g, &tr, &b, &e, &ov, &op, &ks, &save, &internal, &gj, &grid_min, &prof};
     err = cudaLaunchCooperativeKernel((const void*)fn, dim3(G), dim3(32 * kTraceNW), args, smem, st);
   } else {
-    fn<<<1, 32 * kTraceNW, smem, st>>>(g, tr, b, e, ov, op, ks, save, internal, gj, grid_min);
+    fn<<<1, 32 * kTraceNW, smem, st>>>(g, tr, b, e, ov, op, ks, save, internal, gj, grid_min,
+                                       prof);
     err = cudaGetLastError();
   }
   g_launches++;
@@ -351,7 +352,8 @@ struct DevHeap {
   pbh_heap_dev hd{};     // host mirror of the header (pointers + caps)
   pbh_heap_dev* dev = nullptr;  // header in HBM (standalone) or slot in an array
   std::vector<void*> allocs;
-  u32 bc = 0;  // batch capacity (pow2)
+  u32 bc = 0;     // batch capacity (pow2)
+  u64 base1 = 0;  // level-1 bucket capacity (level i >= 1: base1 * 4^(i-1))
 
   pbh_status alloc(void** p, size_t bytes) {
     CK(cudaMalloc(p, bytes ? bytes : 16));
@@ -366,7 +368,7 @@ struct DevHeap {
 
 pbh_status alloc_level(DevHeap& H, u32 i) {
   pbh_level_bufs& b = H.hd.lv[i];
-  const u64 cap = i == 0 ? H.hd.cap0 : (u64)H.hd.cap0 << (2 * i);
+  const u64 cap = i == 0 ? H.hd.cap0 : (u64)H.base1 << (2 * (i - 1));
   if (cap >= (1ull << 31)) return set_err(PBH_OOM, "level capacity exceeds the 2^31 element limit");
   b.cap_b = (u32)cap;
   b.buf_s = i == 0 ? 0 : (u32)cap;
@@ -412,6 +414,7 @@ pbh_status init_heap(DevHeap& H, u64 d, u32 cap0, u32 bc, u32 nt, u64 universe, 
   std::memset(&H.hd, 0, sizeof(H.hd));
   H.hd.d = (u32)std::min<u64>(d, 0xffffffffu);
   H.hd.cap0 = cap0;
+  if (H.base1 == 0) H.base1 = 4ull * cap0;
   H.hd.debug_checks = debug ? 1 : 0;
   for (u32 i = 0; i < PBH_MAX_LEVELS; ++i) H.hd.st[i].spl_inf = 1;
   pbh_status st;
@@ -484,6 +487,7 @@ struct pbh_heap {
   bool bank = true;             // banked level-0 interpreter (false: sorted-B_0 CTA engine)
   TraceImage* d_save = nullptr; // its level-0 image between launches
   u32 grid_min = kGridMin;
+  unsigned long long* d_prof = nullptr;  // PBH_PROF: leader cycle breakdown
   // staging for host traces
   u64 st_ops = 0, st_el = 0, st_out = 0;
   u8* d_kinds = nullptr;
@@ -557,7 +561,7 @@ pbh_status exec_trace(pbh_heap* h, u64 n_ops, pbh_trace_dev tr, u32* d_ov, u64* 
     CK(cudaEventRecord(h->ev0, h->stream));
     if (h->bank) {
       CK(launch_trace_bank(h->stream, h->H.dev, tr, begin, n_ops, d_ov, d_op, h->d_ks, h->d_save,
-                           internal, h->d_job, h->grid_min));
+                           internal, h->d_job, h->grid_min, h->d_prof));
     } else {
       CK(launch_trace_nt(h->nt, h->layout, h->stream, h->H.dev, tr, begin, n_ops, d_ov, d_op,
                          h->d_ks, internal, h->d_job));
@@ -690,7 +694,14 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
   };
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(set_err(PBH_CUDA, "stream create failed"));
-  pbh_status st = init_heap(h->H, d, cap0, bc, h->nt, key_universe, debug_checks, 2, nullptr);
+  // the banked engine pre-allocates levels for the key universe (each
+  // NEED_GROW is a kernel exit + relaunch)
+  u32 nlev = 2;
+  if (h->bank) {
+    h->H.base1 = 4ull * kBankQ;  // level 1 holds four push-buffer flushes
+    while (nlev < 12 && (h->H.base1 << (2 * (nlev - 2))) < 2 * key_universe + 4 * kBankQ) ++nlev;
+  }
+  pbh_status st = init_heap(h->H, d, cap0, bc, h->nt, key_universe, debug_checks, nlev, nullptr);
   if (st) return fail(st);
   h->layout = make_layout(h->nt, cap0, h->H.bc, h->H.hd.d, false);
   if (cudaMalloc(&h->d_ks, sizeof(pbh_kstatus)) != cudaSuccess ||
@@ -711,6 +722,8 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
     if (e != cudaSuccess) return fail(set_err(PBH_CUDA, "level-0 image init failed"));
   }
   if (const char* e = getenv("PBH_GRID_MIN")) h->grid_min = std::max(2, atoi(e));
+  if (getenv("PBH_PROF") && cudaMalloc(&h->d_prof, 16 * sizeof(unsigned long long)) == cudaSuccess)
+    cudaMemset(h->d_prof, 0, 16 * sizeof(unsigned long long));
   cudaEventCreate(&h->ev0);
   cudaEventCreate(&h->ev1);
   *out = h;
@@ -726,6 +739,15 @@ pbh_status pbh_heap_destroy(pbh_heap* h) {
   cudaFreeHost(h->h_ks);
   cudaFree(h->d_job);
   cudaFree(h->d_save);
+  if (h->d_prof) {
+    unsigned long long pc[16];
+    cudaMemcpy(pc, h->d_prof, sizeof pc, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "pbh_prof cycles: validate %llu apply %llu bulk_cold %llu extract %llu refill %llu tail %llu pre %llu"
+            " | sort %llu push_down %llu resolve1 %llu r2 %llu r3 %llu r4 %llu r5 %llu r6+ %llu\n",
+            pc[0], pc[1], pc[2], pc[3], pc[4], pc[5], pc[6], pc[8], pc[9], pc[10], pc[11], pc[12],
+            pc[13], pc[14], pc[15]);
+    cudaFree(h->d_prof);
+  }
   cudaFree(h->d_kinds);
   cudaFree(h->d_off);
   cudaFree(h->d_vals);
@@ -1137,6 +1159,7 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
   u32 nlev = 2;
   while (nlev < 8 && ((u64)c->cap0 << (2 * (nlev - 1))) < 8ull * (c->max_deg + 1)) ++nlev;
   for (u64 i = 0; i < max_sources; ++i) {
+    if (c->lane) c->heaps[i].base1 = 4ull * kBankQ;
     st = init_heap(c->heaps[i], c->d, c->cap0, bc, c->nt, std::max<u32>(c->V, 1), 0, nlev,
                    c->d_heaps + i);
     if (st) return fail(st);

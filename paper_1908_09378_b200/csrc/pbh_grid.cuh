@@ -23,6 +23,7 @@ namespace pbh_dev {
 
 constexpr u32 kGridTile = 2048;   // outputs per streamed tile
 constexpr u32 kGridMin = 16384;   // smallest merge worth a grid job
+constexpr u32 kStreamMin = 64;    // smallest merge streamed through the windows by one CTA
 
 // Job word + descriptor in HBM (one per heap handle).
 struct GridJob {
@@ -70,14 +71,18 @@ DEV void grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u
   while (ia < ia_end || ib < ib_end) {
     const u32 na = min(kGridTile, ia_end - ia), nb = min(kGridTile, ib_end - ib);
     const u32 n = min(kGridTile, (ia_end - ia) + (ib_end - ib));
+    // windows straight into shared memory (cp.async: no register round trip,
+    // every load of the tile in flight at once)
     for (u32 i = tid; i < na; i += NT) {
-      g.ak[i] = J.ak[ia + i];
-      g.ap[i] = J.ap[ia + i];
+      cp_async4(&g.ak[i], J.ak + ia + i, true);
+      cp_async8(&g.ap[i], J.ap + ia + i);
     }
     for (u32 i = tid; i < nb; i += NT) {
-      g.bk[i] = J.bk[ib + i];
-      g.bp[i] = J.bp[ib + i];
+      cp_async4(&g.bk[i], J.bk + ib + i, true);
+      cp_async8(&g.bp[i], J.bp + ib + i);
     }
+    cp_async_commit();
+    cp_async_wait_all();
     Bk::sync();
     // this thread's outputs [d0, d1): merge-path split inside the windows
     const u32 d0 = min(tid * VT, n), d1 = min(d0 + VT, n);

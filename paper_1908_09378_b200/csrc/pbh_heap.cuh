@@ -57,17 +57,47 @@ struct HeapCta {
   // helpers cannot see this CTA's shared memory: grid jobs take HBM runs only
   DEV static bool hbm(const void* p) { return p == nullptr || !__isShared(p); }
   DEV static bool hbm_sink(const Sink& k) { return hbm(k.k1) && (k.lim == kInfCount || hbm(k.k2)); }
+  // This CTA alone streams the merge through the GridSmem windows
+  // (unfiltered; cp.async window loads).
+  NOINL void stream_local(const Run& A, const Run& B, const Sink& snk, u32 out_base) {
+    Bk::sync();
+    if (threadIdx.x == 0) {
+      GridJob& J = gs->job;
+      J.ak = A.k;
+      J.ap = A.p;
+      J.bk = B.k;
+      J.bp = B.p;
+      J.na = A.n;
+      J.nb = B.n;
+      J.c = A.n + B.n;
+      J.sink = snk;
+    }
+    Bk::sync();
+    grid_stream<NT>(gs->job, 0, A.n, 0, B.n, out_base, *gs);
+    Bk::sync();
+  }
   NOINL u32 mrg(const Run& A, const Run& B, bool filter, const Sink& snk, u32 out_base) {
     const u32 tot = A.n + B.n;
-    if (gj && tot >= gmin && hbm(A.k) && hbm(B.k) && hbm_sink(snk)) {
+    const bool mem = gs && hbm(A.k) && hbm(B.k) && hbm_sink(snk);
+    if (mem && gj && tot >= gmin) {
       grid_run<NT>(gj, gsz, 0, A, B, tot, snk, out_base, *gs, gs->scr);
+      return tot;
+    }
+    if (mem && tot >= kStreamMin) {
+      stream_local(A, B, snk, out_base);
       return tot;
     }
     return merge_runs<NT, VT>(A, B, filter, idx, snk, out_base, s.tile, scr());
   }
   NOINL u32 cpy(const Run& A, bool filter, const Sink& snk, u32 out_base) {
-    if (gj && A.n >= gmin && hbm(A.k) && hbm_sink(snk)) {
-      grid_run<NT>(gj, gsz, 0, A, Run{A.k, A.p, 0}, A.n, snk, out_base, *gs, gs->scr);
+    const Run E{A.k, A.p, 0};
+    const bool mem = gs && hbm(A.k) && hbm_sink(snk);
+    if (mem && gj && A.n >= gmin) {
+      grid_run<NT>(gj, gsz, 0, A, E, A.n, snk, out_base, *gs, gs->scr);
+      return A.n;
+    }
+    if (mem && A.n >= kStreamMin) {
+      stream_local(A, E, snk, out_base);
       return A.n;
     }
     return copy_run<NT, VT>(A, filter, idx, snk, out_base, scr());
@@ -298,8 +328,10 @@ struct HeapCta {
       // is always refilled here, tile by tile, through the index filter
       const Run A{Bj.k + ha, Bj.p + ha, Bj.n - ha};
       const Run B{Sj.k + hb, Sj.p + hb, adm - hb};
-      const bool on_grid = gj && i > 0 && c >= gmin && hbm(A.k) && hbm(B.k) && hbm_sink(dst);
-      if (!on_grid && c > T) c = T;
+      const bool mem = gs && i > 0 && hbm(A.k) && hbm(B.k) && hbm_sink(dst);
+      const bool on_grid = mem && gj && c >= gmin;
+      const bool streamed = mem && !on_grid && c >= kStreamMin;
+      if (!on_grid && !streamed && c > T) c = T;
       const u32 a = merge_split<NT>(A, B, c, scr());
       // last element of the tile in merged order
       {
@@ -316,6 +348,10 @@ struct HeapCta {
       }
       if (on_grid) {
         grid_run<NT>(gj, gsz, 0, A, B, c, dst, n, *gs, gs->scr);
+        n += c;
+      } else if (streamed) {
+        const u32 a_c = a;  // first c outputs = A[0, a) + B[0, c - a)
+        stream_local(Run{A.k, A.p, a_c}, Run{B.k, B.p, c - a_c}, dst, n);
         n += c;
       } else {
         n += merge_tile<NT, VT>(A, 0, a, B, 0, c - a, true, idx, dst, n, s.tile, scr());

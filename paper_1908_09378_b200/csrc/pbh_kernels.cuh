@@ -70,10 +70,10 @@ __global__ void __launch_bounds__(NT) k_trace(pbh_heap_dev* g, pbh_trace_dev tr,
   }
   typename HC::Sm& sm = *reinterpret_cast<typename HC::Sm*>(dyn);
   HC h{sm};
+  h.gs = &gsm;  // streamed CTA-local merges
   if (gridDim.x > 1) {
     h.gj = gj;
     h.gsz = gridDim.x;
-    h.gs = &gsm;
     h.gmin = L.grid_min;
     grid_leader_init<NT>(gsm);
   }

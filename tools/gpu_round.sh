@@ -1,3 +1,5 @@
 set -x
-for gm in 256 1024 4096 16384; do PBH_GRID_MIN=$gm timeout 600 python tools/probe_trace.py c1 fill > gpurun_out/trace_gm$gm.log 2>&1; done
-tail -n 5 gpurun_out/trace_gm*.log | cut -c1-200
+timeout 600 python -m pytest tests/test_heap_gpu.py tests/test_sssp_gpu.py -x -q > gpurun_out/pytest_hs.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_hs.log
+PBH_PROF=1 timeout 600 python tools/probe_trace.py c1 fill > gpurun_out/tprof.log 2>&1
+timeout 300 python tools/probe.py band_small grid_small > gpurun_out/probe.log 2>&1
+tail -n 3 gpurun_out/pytest_hs.log; cat gpurun_out/tprof.log gpurun_out/probe.log | cut -c1-300
