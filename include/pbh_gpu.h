@@ -160,6 +160,12 @@ pbh_status pbh_sssp_ctx_fetch(pbh_sssp_ctx* c, uint64_t source_slot, uint64_t* d
                               uint64_t* rounds, uint64_t* ops);
 pbh_status pbh_sssp_ctx_destroy(pbh_sssp_ctx* c);
 
+/* Page-lock a caller-owned host range (cudaHostRegister, portable) so the
+ * CSR uploads and result downloads of pbh_sssp / pbh_sssp_multi run at DMA
+ * speed; no reference counterpart (the reference is host-only). */
+pbh_status pbh_host_register(void* ptr, uint64_t bytes);
+pbh_status pbh_host_unregister(void* ptr);
+
 /* distance_checksum (sssp.cpp:174-183): FNV-1a over the distance bytes. */
 uint64_t pbh_distance_checksum(const uint64_t* dist, uint64_t n);
 

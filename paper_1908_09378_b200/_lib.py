@@ -57,6 +57,8 @@ SIGNATURES = {
     "pbh_sssp_ctx_fetch": (C.c_int, [C.c_void_p, C.c_uint64, U64P, U32P, U32P, U64P, U64P, U64P]),
     "pbh_sssp_ctx_destroy": (C.c_int, [C.c_void_p]),
     "pbh_distance_checksum": (C.c_uint64, [U64P, C.c_uint64]),
+    "pbh_host_register": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "pbh_host_unregister": (C.c_int, [C.c_void_p]),
 }
 
 _lib = None

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -355,7 +356,26 @@ struct DevHeap {
   u32 bc = 0;     // batch capacity (pow2)
   u64 base1 = 0;  // level-1 bucket capacity (level i >= 1: base1 * 4^(i-1))
 
+  // Optional arena (one cudaMalloc for many heaps: an SSSP context holds
+  // one heap per source), and a measuring mode that only sums the sizes.
+  char* arena = nullptr;
+  size_t arena_cap = 0, arena_used = 0;
+  bool measure = false;
+  size_t measured = 0;
+  static size_t a256(size_t b) { return (std::max<size_t>(b, 16) + 255) & ~size_t(255); }
+
   pbh_status alloc(void** p, size_t bytes) {
+    const size_t b = a256(bytes);
+    if (measure) {
+      measured += b;
+      *p = reinterpret_cast<void*>(size_t(256));
+      return PBH_OK;
+    }
+    if (arena && arena_used + b <= arena_cap) {
+      *p = arena + arena_used;
+      arena_used += b;
+      return PBH_OK;
+    }
     CK(cudaMalloc(p, bytes ? bytes : 16));
     allocs.push_back(*p);
     return PBH_OK;
@@ -391,7 +411,7 @@ pbh_status alloc_level(DevHeap& H, u32 i) {
   return PBH_OK;
 }
 
-pbh_status alloc_scratch(DevHeap& H, u32 bc, u32 nt) {
+pbh_status alloc_scratch(DevHeap& H, u32 bc, u32 nt, cudaStream_t strm = 0) {
   pbh_status st;
   H.bc = bc;
   if ((st = H.alloc((void**)&H.hd.g_bk, (u64)bc * 4))) return st;
@@ -399,7 +419,7 @@ pbh_status alloc_scratch(DevHeap& H, u32 bc, u32 nt) {
   if ((st = H.alloc((void**)&H.hd.g_pk, (u64)bc * 4))) return st;
   if ((st = H.alloc((void**)&H.hd.g_pp, (u64)bc * 8))) return st;
   if ((st = H.alloc((void**)&H.hd.g_rm, H.hd.cap0))) return st;
-  CK(cudaMemset(H.hd.g_rm, 0, H.hd.cap0));
+  if (!H.measure) CK(cudaMemsetAsync(H.hd.g_rm, 0, H.hd.cap0, strm));
   const u64 cc = (u64)H.hd.d + nt;
   if ((st = H.alloc((void**)&H.hd.g_ck, cc * 4))) return st;
   if ((st = H.alloc((void**)&H.hd.g_cp, cc * 8))) return st;
@@ -410,7 +430,7 @@ pbh_status alloc_scratch(DevHeap& H, u32 bc, u32 nt) {
 
 // Initialise a heap: header, n_levels levels, scratch, index of `universe`.
 pbh_status init_heap(DevHeap& H, u64 d, u32 cap0, u32 bc, u32 nt, u64 universe, int debug,
-                     u32 n_levels, pbh_heap_dev* dev_slot) {
+                     u32 n_levels, pbh_heap_dev* dev_slot, cudaStream_t strm = 0) {
   std::memset(&H.hd, 0, sizeof(H.hd));
   H.hd.d = (u32)std::min<u64>(d, 0xffffffffu);
   H.hd.cap0 = cap0;
@@ -420,16 +440,18 @@ pbh_status init_heap(DevHeap& H, u64 d, u32 cap0, u32 bc, u32 nt, u64 universe, 
   pbh_status st;
   for (u32 i = 0; i < n_levels; ++i)
     if ((st = alloc_level(H, i))) return st;
-  if ((st = alloc_scratch(H, bc, nt))) return st;
+  if ((st = alloc_scratch(H, bc, nt, strm))) return st;
   H.hd.universe = universe;
   if ((st = H.alloc((void**)&H.hd.idx, universe * sizeof(pbh_idx_entry)))) return st;
-  CK(cudaMemset(H.hd.idx, 0xff, universe * sizeof(pbh_idx_entry)));
   if (dev_slot) {
     H.dev = dev_slot;
   } else {
     if ((st = H.alloc((void**)&H.dev, sizeof(pbh_heap_dev)))) return st;
   }
-  CK(cudaMemcpy(H.dev, &H.hd, sizeof(pbh_heap_dev), cudaMemcpyHostToDevice));
+  if (H.measure) return PBH_OK;
+  CK(cudaMemsetAsync(H.hd.idx, 0xff, universe * sizeof(pbh_idx_entry), strm));
+  CK(cudaMemcpyAsync(H.dev, &H.hd, sizeof(pbh_heap_dev), cudaMemcpyHostToDevice, strm));
+  if (strm == 0) CK(cudaStreamSynchronize(0));
   return PBH_OK;
 }
 
@@ -1155,15 +1177,30 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
       (st = ctx_alloc(c, (void**)&c->d_save, max_sources * bank_save_bytes_nw(c->bank_nw))))
     return fail(st);
   c->heaps.resize(max_sources);
+  // one arena for every source's heap (levels, scratch, index)
   // initial levels: enough for a few rows of relaxations
   u32 nlev = 2;
   while (nlev < 8 && ((u64)c->cap0 << (2 * (nlev - 1))) < 8ull * (c->max_deg + 1)) ++nlev;
+  size_t per_heap = 0;
+  {
+    DevHeap M;
+    M.measure = true;
+    if (c->lane) M.base1 = 4ull * kBankQ;
+    init_heap(M, c->d, c->cap0, bc, c->nt, std::max<u32>(c->V, 1), 0, nlev, c->d_heaps);
+    per_heap = M.measured;
+  }
+  char* arena = nullptr;
+  if ((st = ctx_alloc(c, (void**)&arena, per_heap * max_sources))) return fail(st);
   for (u64 i = 0; i < max_sources; ++i) {
-    if (c->lane) c->heaps[i].base1 = 4ull * kBankQ;
-    st = init_heap(c->heaps[i], c->d, c->cap0, bc, c->nt, std::max<u32>(c->V, 1), 0, nlev,
-                   c->d_heaps + i);
+    DevHeap& H = c->heaps[i];
+    if (c->lane) H.base1 = 4ull * kBankQ;
+    H.arena = arena + per_heap * i;
+    H.arena_cap = per_heap;
+    st = init_heap(H, c->d, c->cap0, bc, c->nt, std::max<u32>(c->V, 1), 0, nlev, c->d_heaps + i,
+                   c->stream);
     if (st) return fail(st);
   }
+  CK(cudaStreamSynchronize(c->stream));
   *out = c;
   return PBH_OK;
 }
@@ -1327,13 +1364,25 @@ pbh_status pbh_sssp_multi(const pbh_csr* g, const uint32_t* sources, uint64_t n_
     if (b >= e) continue;
     th.emplace_back([&, r, b, e] {
       pbh_sssp_ctx* c = nullptr;
+      const bool prof = getenv("PBH_E2E_PROF") != nullptr;
+      auto now = [] { return std::chrono::steady_clock::now(); };
+      auto t0 = now();
       pbh_status st = pbh_sssp_ctx_create(g, d, devices[r], e - b, &c);
+      auto t1 = now();
       if (!st) st = pbh_sssp_ctx_run(c, sources + b, e - b, 0, nullptr);
+      auto t2 = now();
       for (u64 i = b; !st && i < e; ++i)
         st = pbh_sssp_ctx_fetch(c, i - b, dist + i * g->vertex_count,
                                 parent ? parent + i * g->vertex_count : nullptr, nullptr, nullptr,
                                 nullptr, nullptr);
+      auto t3 = now();
       if (c) pbh_sssp_ctx_destroy(c);
+      auto t4 = now();
+      if (prof) {
+        auto ms = [](auto a, auto z) { return std::chrono::duration<double, std::milli>(z - a).count(); };
+        fprintf(stderr, "pbh_sssp_multi dev %d: create %.1f ms run %.1f ms fetch %.1f ms destroy %.1f ms\n",
+                devices[r], ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
+      }
       res[r] = st;
       if (st) msg[r] = g_last_error;
     });
@@ -1341,6 +1390,18 @@ pbh_status pbh_sssp_multi(const pbh_csr* g, const uint32_t* sources, uint64_t n_
   for (auto& t : th) t.join();
   for (int r = 0; r < n_devices; ++r)
     if (res[r]) return set_err(res[r], msg[r]);
+  return PBH_OK;
+}
+
+pbh_status pbh_host_register(void* ptr, uint64_t bytes) {
+  if (!ptr || !bytes) return set_err(PBH_PRECONDITION, "null or empty host range");
+  CK(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
+  return PBH_OK;
+}
+
+pbh_status pbh_host_unregister(void* ptr) {
+  if (!ptr) return set_err(PBH_PRECONDITION, "null host pointer");
+  CK(cudaHostUnregister(ptr));
   return PBH_OK;
 }
 

@@ -72,15 +72,21 @@ def par_dijkstra(g, source: int, d: int = 0, dag_mode: bool = False, device: int
     return SsspResult(dist[:V], settled[:ns.value], nr.value, ops.value, parent[:V])
 
 
-def par_dijkstra_multi(g, sources, d: int = 0, devices=(0,)):
+def par_dijkstra_multi(g, sources, d: int = 0, devices=(0,), out=None):
     """Independent sources dealt contiguously over ``devices`` (BASELINE C5).
-    Returns (dist[n_sources, V], parent[n_sources, V])."""
+    Returns (dist[n_sources, V], parent[n_sources, V]); ``out`` may supply
+    those two arrays (e.g. page-locked with :func:`pin`)."""
     g = CsrGraph.of(g)
     cs = g.c_struct()
     src = np.ascontiguousarray(sources, dtype=np.uint32)
     devs = (C.c_int * len(devices))(*devices)
-    dist = np.zeros((len(src), g.vertex_count), np.uint64)
-    parent = np.zeros((len(src), g.vertex_count), np.uint32)
+    if out is None:
+        dist = np.zeros((len(src), g.vertex_count), np.uint64)
+        parent = np.zeros((len(src), g.vertex_count), np.uint32)
+    else:
+        dist, parent = out
+        assert dist.shape == (len(src), g.vertex_count) and dist.dtype == np.uint64
+        assert parent.shape == (len(src), g.vertex_count) and parent.dtype == np.uint32
     raise_for(_lib.lib().pbh_sssp_multi(C.byref(cs), src.ctypes.data_as(_lib.U32P), len(src), d,
                                         devs, len(devices), dist.ctypes.data_as(_lib.U64P),
                                         parent.ctypes.data_as(_lib.U32P)))
@@ -181,3 +187,14 @@ def validate_parent_tree(g, source, dist, parent) -> str | None:
     if not np.all(dist[par] + w[a] == dist[vs]):
         return "dist[v] != dist[parent] + w"
     return None
+
+
+def pin(*arrays):
+    """Page-lock numpy arrays for fast host<->device copies (pbh_host_register)."""
+    for a in arrays:
+        raise_for(_lib.lib().pbh_host_register(C.c_void_p(a.ctypes.data), a.nbytes))
+
+
+def unpin(*arrays):
+    for a in arrays:
+        raise_for(_lib.lib().pbh_host_unregister(C.c_void_p(a.ctypes.data)))

@@ -1,5 +1,5 @@
 set -x
-timeout 600 python -m pytest tests/test_heap_gpu.py tests/test_sssp_gpu.py -x -q > gpurun_out/pytest_hs.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_hs.log
-PBH_PROF=1 timeout 600 python tools/probe_trace.py c1 fill > gpurun_out/tprof.log 2>&1
-timeout 300 python tools/probe.py band_small grid_small > gpurun_out/probe.log 2>&1
-tail -n 3 gpurun_out/pytest_hs.log; cat gpurun_out/tprof.log gpurun_out/probe.log | cut -c1-300
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_bytes.sum --clock-control none -k regex:k_sssp_bank --launch-skip 2 -c 1 --csv --log-file gpurun_out/bank_c5_dram.csv python tools/probe.py band band64 > gpurun_out/bank_c5_dram.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bench_ncu.log 2>&1
+cat gpurun_out/bench.log
