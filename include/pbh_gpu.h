@@ -160,6 +160,16 @@ pbh_status pbh_sssp_ctx_fetch(pbh_sssp_ctx* c, uint64_t source_slot, uint64_t* d
                               uint64_t* rounds, uint64_t* ops);
 pbh_status pbh_sssp_ctx_destroy(pbh_sssp_ctx* c);
 
+/* bellman_ford (sssp.hpp:37, sssp.cpp:99-129) on the device: a frontier
+ * label-correcting sweep (one cooperative grid, 64-bit atomicMin), the
+ * baseline the bucket heap is compared with. Distances are
+ * the exact shortest-path distances; parent (optional) is a valid
+ * shortest-path tree recovered from tight edges, parent[source] = source;
+ * rounds = frontier iterations (the reference counts full sweeps). */
+pbh_status pbh_bellman_ford(const pbh_csr* g, uint32_t source, int device, uint64_t* dist,
+                            uint32_t* parent, uint64_t* rounds, uint64_t* edges_scanned,
+                            double* device_ms);
+
 /* Page-lock a caller-owned host range (cudaHostRegister, portable) so the
  * CSR uploads and result downloads of pbh_sssp / pbh_sssp_multi run at DMA
  * speed; no reference counterpart (the reference is host-only). */

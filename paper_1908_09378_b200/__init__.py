@@ -7,6 +7,6 @@ reference's C++ interface used by tests and the benchmark.
 from .errors import (DeviceError, EmptyHeapError, InvariantError, PreconditionError,  # noqa: F401
                      TraceError)
 from .heap import Element, Engine, EngineConfig, Metrics, RunResult  # noqa: F401
-from .sssp import (K_INF_DIST, CsrGraph, SsspContext, SsspResult, distance_checksum,  # noqa: F401
+from .sssp import (K_INF_DIST, CsrGraph, bellman_ford, SsspContext, SsspResult, distance_checksum,  # noqa: F401
                    distances_to_csv, par_dijkstra, par_dijkstra_multi, pin, unpin,
                    validate_parent_tree)

@@ -17,6 +17,7 @@
 #include "../../include/pbh_gpu.h"
 #include "pbh_fast.cuh"
 #include "pbh_bank.cuh"
+#include "pbh_bf.cuh"
 
 using namespace pbh_dev;
 
@@ -1391,6 +1392,87 @@ pbh_status pbh_sssp_multi(const pbh_csr* g, const uint32_t* sources, uint64_t n_
   for (int r = 0; r < n_devices; ++r)
     if (res[r]) return set_err(res[r], msg[r]);
   return PBH_OK;
+}
+
+pbh_status pbh_bellman_ford(const pbh_csr* g, uint32_t source, int device, uint64_t* dist,
+                            uint32_t* parent, uint64_t* rounds, uint64_t* edges_scanned,
+                            double* device_ms) {
+  if (!g || !dist) return set_err(PBH_PRECONDITION, "bad arguments");
+  if (source >= g->vertex_count) return set_err(PBH_PRECONDITION, "bellman_ford: source out of range");
+  CK(cudaSetDevice(device));
+  const u64 V = g->vertex_count, E = g->edge_count;
+  std::vector<void*> mem;
+  auto fin = [&](pbh_status st) {
+    for (void* p : mem) cudaFree(p);
+    return st;
+  };
+  auto dalloc = [&](void** p, size_t b) -> bool {
+    if (cudaMalloc(p, b ? b : 16) != cudaSuccess) return false;
+    mem.push_back(*p);
+    return true;
+  };
+  u64 *d_off = nullptr, *d_dist = nullptr;
+  u32 *d_tgt = nullptr, *d_w = nullptr, *fq0 = nullptr, *fq1 = nullptr, *stamp = nullptr, *d_par = nullptr;
+  BfState* d_st = nullptr;
+  if (!dalloc((void**)&d_off, (V + 1) * 8) || !dalloc((void**)&d_tgt, E * 4) ||
+      !dalloc((void**)&d_w, E * 4) || !dalloc((void**)&d_dist, V * 8) ||
+      !dalloc((void**)&fq0, V * 4) || !dalloc((void**)&fq1, V * 4) ||
+      !dalloc((void**)&stamp, V * 4) || !dalloc((void**)&d_st, sizeof(BfState)) ||
+      (parent && !dalloc((void**)&d_par, V * 4)))
+    return fin(set_err(PBH_OOM, "bellman_ford: device allocation failed"));
+  cudaStream_t st = nullptr;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaMemcpyAsync(d_off, g->offsets, (V + 1) * 8, cudaMemcpyHostToDevice, st);
+  if (E) {
+    cudaMemcpyAsync(d_tgt, g->targets, E * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_w, g->weights, E * 4, cudaMemcpyHostToDevice, st);
+  }
+  cudaMemsetAsync(d_dist, 0xff, V * 8, st);
+  cudaMemsetAsync(d_dist + source, 0, 8, st);
+  cudaMemsetAsync(stamp, 0, V * 4, st);
+  BfState h0{};
+  h0.cnt[0] = 1;
+  cudaMemcpyAsync(d_st, &h0, sizeof h0, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(fq0, &source, 4, cudaMemcpyHostToDevice, st);
+  int sms = 0, per = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_bellman_ford, 256, 0);
+  const int G = std::max(1, sms * std::max(1, std::min(per, 4)));
+  u32 Vv = (u32)V;
+  u64 max_it = V + 1;
+  void* args[] = {&d_off, &d_tgt, &d_w, &Vv, &d_dist, &fq0, &fq1, &stamp, &d_st, &max_it};
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  cudaError_t err = cudaLaunchCooperativeKernel((const void*)k_bellman_ford, dim3(G), dim3(256), args, 0, st);
+  g_launches++;
+  cudaEventRecord(e1, st);
+  if (err == cudaSuccess && parent) {
+    cudaMemsetAsync(d_par, 0xff, V * 4, st);
+    k_bf_parents<<<sms * 8, 256, 0, st>>>(d_off, d_tgt, d_w, Vv, d_dist, d_par);
+    g_launches++;
+    err = cudaGetLastError();
+  }
+  BfState hs{};
+  if (err == cudaSuccess) {
+    cudaMemcpyAsync(&hs, d_st, sizeof hs, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(dist, d_dist, V * 8, cudaMemcpyDeviceToHost, st);
+    if (parent) cudaMemcpyAsync(parent, d_par, V * 4, cudaMemcpyDeviceToHost, st);
+    err = cudaStreamSynchronize(st);
+  }
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(st);
+  if (err != cudaSuccess) return fin(set_err(PBH_CUDA, std::string("bellman_ford: ") + cudaGetErrorString(err)));
+  if (hs.status == 9) return fin(set_err(PBH_INVARIANT, "sssp: distance accumulation overflow"));
+  if (parent) parent[source] = source;
+  if (rounds) *rounds = hs.iters;
+  if (edges_scanned) *edges_scanned = hs.relaxed;
+  if (device_ms) *device_ms = ms;
+  return fin(PBH_OK);
 }
 
 pbh_status pbh_host_register(void* ptr, uint64_t bytes) {

@@ -72,6 +72,27 @@ def par_dijkstra(g, source: int, d: int = 0, dag_mode: bool = False, device: int
     return SsspResult(dist[:V], settled[:ns.value], nr.value, ops.value, parent[:V])
 
 
+def bellman_ford(g, source: int, device: int = 0, with_parent: bool = True):
+    """bellman_ford (sssp.hpp:37; sssp.cpp:99-129) as a device frontier sweep.
+    Returns (SsspResult with settled_order = reached vertices by (dist, vid),
+    edges_scanned, device_ms); ``rounds`` counts frontier iterations."""
+    g = CsrGraph.of(g)
+    cs = g.c_struct()
+    V = g.vertex_count
+    dist = np.zeros(max(V, 1), np.uint64)
+    parent = np.zeros(max(V, 1), np.uint32) if with_parent else None
+    nr, ne, ms = C.c_uint64(), C.c_uint64(), C.c_double()
+    raise_for(_lib.lib().pbh_bellman_ford(
+        C.byref(cs), int(source), device, dist.ctypes.data_as(_lib.U64P),
+        parent.ctypes.data_as(_lib.U32P) if with_parent else None, C.byref(nr), C.byref(ne),
+        C.byref(ms)))
+    d = dist[:V]
+    reached = np.nonzero(d != K_INF_DIST)[0].astype(np.uint32)
+    order = reached[np.lexsort((reached, d[reached]))]
+    return (SsspResult(d, order, nr.value, 0, parent[:V] if with_parent else None),
+            ne.value, ms.value)
+
+
 def par_dijkstra_multi(g, sources, d: int = 0, devices=(0,), out=None):
     """Independent sources dealt contiguously over ``devices`` (BASELINE C5).
     Returns (dist[n_sources, V], parent[n_sources, V]); ``out`` may supply

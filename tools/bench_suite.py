@@ -94,6 +94,20 @@ def sssp_rec(name, g, cpu_graph_fn):
     return rec
 
 
+def bf_rec(name, g, heap_ms=None):
+    """Device Bellman-Ford (frontier sweep) on the same graph as a heap config
+    (heap vs sweep on dense high-diameter graphs)."""
+    r, scanned, ms = P.bellman_ford(g, 0, with_parent=False)
+    E = g.edge_count
+    rec = {"config": name, "device_ms": ms, "frontier_iterations": r.rounds,
+           "edges_scanned": scanned, "scan_over_E": scanned / max(E, 1),
+           "edges_per_s": E / (ms / 1e3), "checksum": P.distance_checksum(r.dist)}
+    if heap_ms:
+        rec["heap_device_ms"] = heap_ms
+        rec["heap_speedup_over_bf"] = ms / heap_ms
+    return rec
+
+
 def c4(log2n, ds, batches_per_d):
     n = 1 << log2n
     pr = gen.sweep_prefill(n, 4)
@@ -156,6 +170,17 @@ def main():
             return O.gen_grid(1024, 1024, 1), "1024x1024 grid (1/16 of C2), 1 thread"
         res["c2"] = sssp_rec("C2 grid SSSP", g, small)
         print(json.dumps(res["c2"]), file=sys.stderr, flush=True)
+        del g
+    if "bf" in args.which:
+        g = gen.band(1 << 20, 256, 2)
+        res["bf_c3"] = bf_rec("Bellman-Ford on the C3 band", g,
+                              res.get("c3", {}).get("device_ms"))
+        print(json.dumps(res["bf_c3"]), file=sys.stderr, flush=True)
+        del g
+        g = gen.grid(4096, 4096, 1)
+        res["bf_c2"] = bf_rec("Bellman-Ford on the C2 grid", g,
+                              res.get("c2", {}).get("device_ms"))
+        print(json.dumps(res["bf_c2"]), file=sys.stderr, flush=True)
         del g
     if "c4" in args.which:
         ds = [int(x) for x in args.c4_ds.split(",")]
