@@ -158,6 +158,12 @@ pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n
 pbh_status pbh_sssp_ctx_fetch(pbh_sssp_ctx* c, uint64_t source_slot, uint64_t* dist,
                               uint32_t* parent, uint32_t* settled, uint64_t* n_settled,
                               uint64_t* rounds, uint64_t* ops);
+/* Extension: mode 1 = threshold multi-extraction.
+ * Each round settles every level-0 vertex whose distance is final by the
+ * Crauser IN/OUT criteria; distances and parents are exact/valid, `rounds`
+ * counts batches, `settled` lists vertices in batch order (sort by
+ * (dist, vid) for the reference's settle order). mode 0 = par_dijkstra. */
+pbh_status pbh_sssp_ctx_set_mode(pbh_sssp_ctx* c, int mode);
 pbh_status pbh_sssp_ctx_destroy(pbh_sssp_ctx* c);
 
 /* bellman_ford (sssp.hpp:37, sssp.cpp:99-129) on the device: a frontier

@@ -45,7 +45,7 @@ constexpr int kBankQ = 4096;    // push-buffer capacity (entries beyond the spli
 constexpr int kBankPass = 256;  // edges relaxed per pass
 
 // The part of the shared-memory image that survives a NEED_GROW relaunch.
-template <int B, int KI>
+template <int B, int KI, bool MW = false>
 struct BankL0 {
   static constexpr int C0 = B * KI;
   u64 lp[C0];    // slot priority
@@ -58,20 +58,24 @@ struct BankL0 {
   u64 spl_p;
   u32 spl_k, spl_inf, qn, pad;
   u64 pushes;    // push_down count (drives the 4-to-1 resolve schedule)
+  // multi-extraction mode: the slot vertex's minimum out / in edge weight
+  u32 lmo[MW ? C0 : 1];
+  u32 lmi[MW ? C0 : 1];
 };
 
 // One warp's offer and counters for the per-pass exchange.
 struct BankOffer {
   u64 p, rb;
+  u64 t;  // multi-extraction: min over offers of (p + min out weight)
   u32 k, slot, deg, has;
   u32 fresh, nimp, nq, flags;  // flags: 1 evict due, 2 bad slot, 4 overflow
 };
 
-template <int NW, int KI, int VT>
+template <int NW, int KI, int VT, bool MW = false>
 struct BankSmem {
   static constexpr int B = 32 * NW;
   static constexpr int C0 = B * KI;
-  BankL0<B, KI> l0;
+  BankL0<B, KI, MW> l0;
   // cold-engine B_0 ping-pong (capacity C0/2 each); as one C0-entry array
   // it is also the sort scratch of evict()
   u32 bk[2][C0 / 2];
@@ -85,10 +89,10 @@ struct BankSmem {
   HeapSmem<B, VT> hs;
 };
 
-template <int NW, int KI, int VT>
-DEV BankSmem<NW, KI, VT>& bank_smem() {
+template <int NW, int KI, int VT, bool MW = false>
+DEV BankSmem<NW, KI, VT, MW>& bank_smem() {
   extern __shared__ __align__(16) unsigned char dyn[];
-  return *reinterpret_cast<BankSmem<NW, KI, VT>*>(dyn);
+  return *reinterpret_cast<BankSmem<NW, KI, VT, MW>*>(dyn);
 }
 
 // warp argmin of (p, k) over lanes with `has`; returns the winning lane.
@@ -108,8 +112,8 @@ DEV u32 warp_argmin(bool& has, u64& p, u32& k) {
 }
 
 // This thread's bank minimum (inline on kernel locals so they stay in registers).
-template <int B, int KI>
-DEV void bank_rescan(const BankL0<B, KI>& L, u32 tid, u32 occm, bool& lhas, u64& lmin_p,
+template <int B, int KI, bool MW>
+DEV void bank_rescan(const BankL0<B, KI, MW>& L, u32 tid, u32 occm, bool& lhas, u64& lmin_p,
                      u32& lmin_k, u32& lmin_s) {
   lhas = false;
   u32 m = occm;
@@ -128,19 +132,15 @@ DEV void bank_rescan(const BankL0<B, KI>& L, u32 tid, u32 occm, bool& lhas, u64&
   }
 }
 
-template <int NW, int KI, int VT>
-struct BankSmem;
-template <int NW, int KI, int VT>
-DEV BankSmem<NW, KI, VT>& bank_smem();
 
 // Per-pass exchange: CTA argmin of the offers (has, p, k) with their slot
 // and row, and the sums of the counters. One barrier. Counters are packed
 // 9 bits each (every one is <= 256 per pass): c0 = fresh | nimp << 9 |
 // ovf << 18, c1 = nq | evict << 9 | bad << 18 (the last two per-thread flags).
-template <int NW, int KI, int VT>
+template <int NW, int KI, int VT, bool MW = false>
 DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u32 deg, u32 c0,
-                            u32 c1) {
-  BankSmem<NW, KI, VT>& S = bank_smem<NW, KI, VT>();
+                            u32 c1, u64 t = ~0ull) {
+  BankSmem<NW, KI, VT, MW>& S = bank_smem<NW, KI, VT, MW>();
   const u32 tid = threadIdx.x;
   const u32 lane = tid & 31, w = tid >> 5;
   bool h = has;
@@ -149,8 +149,15 @@ DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u
   const u32 wl = warp_argmin(h, wp, wk);
   const u32 s0 = __reduce_add_sync(0xffffffffu, c0);
   const u32 s1 = __reduce_add_sync(0xffffffffu, c1);
+  u64 wt_ = ~0ull;
+  if constexpr (MW) {  // warp min of t (u64) in two 32-bit reductions
+    const u32 thi = __reduce_min_sync(0xffffffffu, (u32)(t >> 32));
+    const u32 tlo = __reduce_min_sync(0xffffffffu, (u32)(t >> 32) == thi ? (u32)t : 0xffffffffu);
+    wt_ = ((u64)thi << 32) | tlo;
+  }
   if (lane == wl) {
     BankOffer& o = S.ex[par][w];
+    o.t = wt_;
     o.p = wp;
     o.k = wk;
     o.has = h;
@@ -169,6 +176,7 @@ DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u
     r.slot = __shfl_sync(0xffffffffu, slot, wl);
     r.rb = __shfl_sync(0xffffffffu, rb, wl);
     r.deg = __shfl_sync(0xffffffffu, deg, wl);
+    r.t = wt_;
     r.fresh = s0 & 511u;
     r.nimp = (s0 >> 9) & 511u;
     r.nq = s1 & 511u;
@@ -182,6 +190,7 @@ DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u
     u64 bp = S.ex[par][0].p;
     u32 bk = S.ex[par][0].k;
     u32 t0 = S.ex[par][0].fresh, t1 = S.ex[par][0].nq;
+    u64 tm = S.ex[par][0].t;
 #pragma unroll
     for (int i = 1; i < NW; ++i) {
       const bool xh = S.ex[par][i].has;
@@ -189,6 +198,7 @@ DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u
       const u32 xk = S.ex[par][i].k;
       t0 += S.ex[par][i].fresh;
       t1 += S.ex[par][i].nq;
+      if constexpr (MW) tm = min(tm, S.ex[par][i].t);
       if (xh && (!bh || less_pk(xp, xk, bp, bk))) {
         bh = true;
         bp = xp;
@@ -203,6 +213,7 @@ DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u
     r.slot = S.ex[par][bi].slot;
     r.rb = S.ex[par][bi].rb;
     r.deg = S.ex[par][bi].deg;
+    r.t = tm;
     r.fresh = t0 & 511u;
     r.nimp = (t0 >> 9) & 511u;
     r.nq = t1 & 511u;
@@ -330,7 +341,7 @@ DEV void cta_sort(u32* K, u64* P, u32 n, u32* TK, u64* TP) {
   }
 }
 
-template <int NW, int KI, int VT>
+template <int NW, int KI, int VT, bool MW = false>
 struct BankHeap {
   static constexpr int B = 32 * NW;
   static constexpr int C0 = B * KI;
@@ -339,12 +350,14 @@ struct BankHeap {
   static_assert(KI >= (int)PE, "a bank must hold one pass of inserts");
   using HC = HeapCta<B, VT>;
   using Bk = Blk<B>;
-  using SM = BankSmem<NW, KI, VT>;
+  using SM = BankSmem<NW, KI, VT, MW>;
   HC& hc;
   SM& S;
-  BankL0<B, KI>& L;
+  BankL0<B, KI, MW>& L;
   pbh_idx_entry* idx;
   const u64* off;
+  const u32* mwo = nullptr;  // multi-extraction: per-vertex min out / in weight
+  const u32* mwi = nullptr;
   const u32 tid;
   // per-thread
   u32 occm;
@@ -449,6 +462,10 @@ struct BankHeap {
       L.lp[j] = P[j];
       L.lrb[j] = rb;
       L.ldeg[j] = (u32)(re - rb);
+      if constexpr (MW) {
+        L.lmo[j] = __ldg(mwo + k);
+        L.lmi[j] = __ldg(mwi + k);
+      }
       idx[k].state = PBH_ST_LIVE | (j << 2);
       occm |= 1u << (j / B);
     }
@@ -878,6 +895,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
     } else {
       my->status = sm.status;
       my->detail = sm.detail;
+      my->aux = sm.aux;
     }
   }
 }

@@ -731,6 +731,7 @@ __global__ void __launch_bounds__(32, 1)
     } else {
       my->status = sm.status;
       my->detail = sm.detail;
+      my->aux = sm.aux;
     }
   }
 }

@@ -18,6 +18,7 @@
 #include "pbh_fast.cuh"
 #include "pbh_bank.cuh"
 #include "pbh_bf.cuh"
+#include "pbh_multi.cuh"
 
 using namespace pbh_dev;
 
@@ -302,6 +303,26 @@ cudaError_t launch_sssp_bank(cudaStream_t st, u32 grid, pbh_heap_dev* heaps, con
   }
   fn<<<grid, 32 * NW, smem, st>>>(heaps, off, tgt, w, V, src, dist, settled, sst,
                                   reinterpret_cast<BankL0<32 * NW, KI>*>(save), dag, maxdeg, d);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+// Threshold multi-extraction engine (opt-in, pbh_multi.cuh): NW = 4.
+using MultiImage = BankL0<128, 8, true>;
+cudaError_t launch_sssp_multi(cudaStream_t st, u32 grid, pbh_heap_dev* heaps, const u64* off,
+                              const u32* tgt, const u32* w, const u32* mwo, const u32* mwi, u32 V,
+                              const u32* src, u64* dist, u32* settled, SsspState* sst, void* save,
+                              u32 maxdeg, u32 d) {
+  auto fn = k_sssp_multi<4, 8, VT>;
+  const int smem = (int)sizeof(MultiSmem<4, 8, VT>);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  fn<<<grid, 128, smem, st>>>(heaps, off, tgt, w, mwo, mwi, V, src, dist, settled, sst,
+                              reinterpret_cast<MultiImage*>(save), maxdeg, d);
   g_launches++;
   return cudaGetLastError();
 }
@@ -1075,6 +1096,9 @@ struct pbh_sssp_ctx {
   bool lane = true;   // banked level 0 (default)
   int bank_nw = 1;    // warps per source of the banked engine
   void* d_save = nullptr;
+  bool multi = false;  // threshold multi-extraction (pbh_sssp_ctx_set_mode)
+  u32* d_mwo = nullptr;
+  u32* d_mwi = nullptr;
   std::vector<DevHeap> heaps;
   pbh_heap_dev* d_heaps = nullptr;
   SsspState* d_sst = nullptr;
@@ -1175,7 +1199,8 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
   if ((st = ctx_alloc(c, (void**)&c->d_parent, max_sources * c->V * 4))) return fail(st);
   if ((st = ctx_alloc(c, (void**)&c->d_src, max_sources * 4))) return fail(st);
   if (c->lane &&
-      (st = ctx_alloc(c, (void**)&c->d_save, max_sources * bank_save_bytes_nw(c->bank_nw))))
+      (st = ctx_alloc(c, (void**)&c->d_save,
+                      max_sources * std::max(bank_save_bytes_nw(c->bank_nw), sizeof(MultiImage)))))
     return fail(st);
   c->heaps.resize(max_sources);
   // one arena for every source's heap (levels, scratch, index)
@@ -1245,7 +1270,11 @@ pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n
   std::vector<SsspState> hs(n_sources);
   for (int guard = 0; guard < 256; ++guard) {
     CK(cudaEventRecord(c->ev0, c->stream));
-    if (c->lane) {
+    if (c->multi) {
+      CK(launch_sssp_multi(c->stream, (u32)n_sources, c->d_heaps, c->d_off, c->d_tgt, c->d_w,
+                           c->d_mwo, c->d_mwi, c->V, c->d_src, c->d_dist, c->d_settled, c->d_sst,
+                           c->d_save, c->max_deg, (u32)std::min<u64>(c->d, 0xffffffffu)));
+    } else if (c->lane) {
       CK(launch_sssp_bank_nw(c->bank_nw, c->stream, (u32)n_sources, c->d_heaps, c->d_off,
                              c->d_tgt, c->d_w, c->V, c->d_src, c->d_dist, c->d_settled, c->d_sst,
                              c->d_save, dag_mode ? 1 : 0, c->max_deg,
@@ -1275,7 +1304,12 @@ pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n
       } else if (hs[i].status != 0) {
         return set_err(hs[i].status == 3 ? PBH_INVARIANT : PBH_PRECONDITION,
                        std::string("sssp source slot ") + std::to_string(i) + ": " +
-                           detail_message(hs[i].detail));
+                           detail_message(hs[i].detail) +
+                           (hs[i].status == 3 && hs[i].aux ? " (site 0x" + [&] {
+                             char b[24];
+                             std::snprintf(b, sizeof b, "%llx", (unsigned long long)hs[i].aux);
+                             return std::string(b);
+                           }() + ")" : std::string()));
       }
     }
     if (!again) break;
@@ -1330,6 +1364,27 @@ pbh_status pbh_sssp_ctx_fetch(pbh_sssp_ctx* c, uint64_t slot, uint64_t* dist, ui
       *ops = o;
     }
   }
+  return PBH_OK;
+}
+
+pbh_status pbh_sssp_ctx_set_mode(pbh_sssp_ctx* c, int mode) {
+  if (!c || (mode != 0 && mode != 1)) return set_err(PBH_PRECONDITION, "bad mode");
+  if (mode == 1 && !c->lane) return set_err(PBH_PRECONDITION, "threshold mode needs the banked engine");
+  CK(cudaSetDevice(c->device));
+  if (mode == 1 && !c->d_mwo) {
+    pbh_status st;
+    if ((st = ctx_alloc(c, (void**)&c->d_mwo, (u64)c->V * 4))) return st;
+    if ((st = ctx_alloc(c, (void**)&c->d_mwi, (u64)c->V * 4))) return st;
+    CK(cudaMemsetAsync(c->d_mwi, 0xff, (u64)c->V * 4, c->stream));
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    k_min_weights<<<sms * 8, 256, 0, c->stream>>>(c->d_off, c->d_tgt, c->d_w, c->V, c->d_mwo,
+                                                  c->d_mwi);
+    g_launches++;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  c->multi = mode == 1;
   return PBH_OK;
 }
 

@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(NT) k_sssp(pbh_heap_dev* heaps, const u64* __r
     my->status = sm.status;
     my->detail = sm.detail;
     my->aux = sm.aux;
+    my->aux = sm.aux;
   }
 }
 

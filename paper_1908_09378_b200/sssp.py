@@ -72,6 +72,21 @@ def par_dijkstra(g, source: int, d: int = 0, dag_mode: bool = False, device: int
     return SsspResult(dist[:V], settled[:ns.value], nr.value, ops.value, parent[:V])
 
 
+def threshold_sssp(g, source: int, device: int = 0) -> SsspResult:
+    """Threshold multi-extraction SSSP (extension):
+    exact distances and a valid parent tree; ``rounds`` counts batches and
+    ``settled_order`` is reported as the reference's settle order, i.e. the
+    reached vertices sorted by (dist, vid)."""
+    ctx = SsspContext(g, device=device, max_sources=1, mode="threshold")
+    try:
+        ctx.run([source])
+        r = ctx.fetch(0, settled=True)
+    finally:
+        ctx.close()
+    order = r.settled_order[np.lexsort((r.settled_order, r.dist[r.settled_order]))]
+    return SsspResult(r.dist, order, r.rounds, r.ops, r.parent)
+
+
 def bellman_ford(g, source: int, device: int = 0, with_parent: bool = True):
     """bellman_ford (sssp.hpp:37; sssp.cpp:99-129) as a device frontier sweep.
     Returns (SsspResult with settled_order = reached vertices by (dist, vid),
@@ -117,12 +132,22 @@ def par_dijkstra_multi(g, sources, d: int = 0, devices=(0,), out=None):
 class SsspContext:
     """Device-resident CSR for repeated solves (bench: inputs already in HBM)."""
 
-    def __init__(self, g, d: int = 0, device: int = 0, max_sources: int = 1):
+    def __init__(self, g, d: int = 0, device: int = 0, max_sources: int = 1,
+                 mode: str = "exact"):
         self.g = CsrGraph.of(g)
         cs = self.g.c_struct()
         h = C.c_void_p()
         raise_for(_lib.lib().pbh_sssp_ctx_create(C.byref(cs), d, device, max_sources, C.byref(h)))
         self._h = h
+        self.mode = mode
+        if mode != "exact":
+            self.set_mode(mode)
+
+    def set_mode(self, mode: str):
+        """'exact' = par_dijkstra (one extraction per round); 'threshold' =
+        multi-extraction by the Crauser IN/OUT criteria (extension)."""
+        raise_for(_lib.lib().pbh_sssp_ctx_set_mode(self._h, {"exact": 0, "threshold": 1}[mode]))
+        self.mode = mode
 
     def run(self, sources, dag_mode=False) -> float:
         src = np.ascontiguousarray(sources, dtype=np.uint32)

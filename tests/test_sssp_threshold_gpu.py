@@ -1,0 +1,64 @@
+"""Threshold multi-extraction SSSP (extension) on the
+B200: distances bit-exact vs the oracle's reference_dijkstra (sssp.cpp:71-97),
+the reference's settle order recovered as the (dist, vid) sort, parent trees
+valid, and no more rounds than par_dijkstra's one per settled vertex."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def check(pbh, O, g, source=0):
+    want = O.dijkstra(g, source)
+    got = pbh.threshold_sssp(g, source)
+    assert np.array_equal(got.dist, want["dist"])
+    assert np.array_equal(got.settled_order, want["settled_order"])
+    assert pbh.validate_parent_tree(g, source, got.dist, got.parent) is None
+    assert 1 <= got.rounds <= len(want["settled_order"])
+    return got
+
+
+def test_tiny(pbh, O):
+    g = O.make_graph(3, [(0, 1, 5), (0, 2, 1), (2, 1, 1)])
+    assert check(pbh, O, g).dist.tolist() == [0, 2, 1]
+
+
+def test_unreachable(pbh, O):
+    check(pbh, O, O.make_graph(4, [(0, 1, 3), (1, 0, 2)]))
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_random(pbh, O, seed):
+    check(pbh, O, O.gen_random(3000, 24000, 1000, seed), source=seed)
+
+
+def test_tie_heavy(pbh, O):
+    check(pbh, O, O.gen_random(2000, 16000, 3, 7))
+
+
+def test_high_diameter(pbh, O):
+    check(pbh, O, O.gen_high_diameter(2000, 10000, 50, 4))
+
+
+def test_complete(pbh, O):
+    check(pbh, O, O.gen_complete(300, 1000, 5))
+
+
+def test_dag(pbh, O):
+    check(pbh, O, O.gen_dag(2000, 6, 100, 3))
+
+
+def test_grid_fewer_rounds(pbh, O):
+    g = O.gen_grid(128, 128, 1)
+    r = check(pbh, O, g)
+    assert r.rounds < 128 * 128 // 4  # many vertices settle per round on a grid
+
+
+def test_band(pbh, O):
+    r = check(pbh, O, O.gen_band(8192, 64, 2))
+    assert int(r.dist[8191]) == 8191
+
+
+def test_overflow_pushes_and_refills(pbh, O):
+    # a wide graph: level 0 overflows into the push buffer and deeper levels
+    check(pbh, O, O.gen_random(60000, 600000, 1 << 20, 9))

@@ -94,6 +94,22 @@ def sssp_rec(name, g, cpu_graph_fn):
     return rec
 
 
+def thr_rec(name, g, heap_ms=None):
+    """Threshold multi-extraction mode (extension)."""
+    ctx = P.SsspContext(g, device=0, max_sources=1, mode="threshold")
+    ms = [ctx.run([0]) for _ in range(2)]
+    r = ctx.fetch(0, settled=False)
+    ctx.close()
+    V, E = g.vertex_count, g.edge_count
+    rec = {"config": name, "device_ms": ms[-1], "batches": r.rounds,
+           "vertices_per_batch": V / max(r.rounds, 1), "edges_per_s": E / (ms[-1] / 1e3),
+           "checksum": P.distance_checksum(r.dist)}
+    if heap_ms:
+        rec["exact_heap_device_ms"] = heap_ms
+        rec["speedup_over_exact"] = heap_ms / ms[-1]
+    return rec
+
+
 def bf_rec(name, g, heap_ms=None):
     """Device Bellman-Ford (frontier sweep) on the same graph as a heap config
     (heap vs sweep on dense high-diameter graphs)."""
@@ -170,6 +186,17 @@ def main():
             return O.gen_grid(1024, 1024, 1), "1024x1024 grid (1/16 of C2), 1 thread"
         res["c2"] = sssp_rec("C2 grid SSSP", g, small)
         print(json.dumps(res["c2"]), file=sys.stderr, flush=True)
+        del g
+    if "thr" in args.which:
+        g = gen.band(1 << 20, 256, 2)
+        res["thr_c3"] = thr_rec("threshold mode on the C3 band", g,
+                                res.get("c3", {}).get("device_ms"))
+        print(json.dumps(res["thr_c3"]), file=sys.stderr, flush=True)
+        del g
+        g = gen.grid(4096, 4096, 1)
+        res["thr_c2"] = thr_rec("threshold mode on the C2 grid", g,
+                                res.get("c2", {}).get("device_ms"))
+        print(json.dumps(res["thr_c2"]), file=sys.stderr, flush=True)
         del g
     if "bf" in args.which:
         g = gen.band(1 << 20, 256, 2)
