@@ -25,8 +25,11 @@ def test_python_mirror_binds_every_symbol():
     from paper_1908_09378_b200 import _lib, gen
     assert set(declared_symbols()) == set(_lib.SIGNATURES)
     assert set(declared_symbols("pbh_gen.h")) == set(gen.GEN_SIGNATURES)
+    from paper_1908_09378_b200 import trace_io
+    assert set(declared_symbols("pbh_trace_io.h")) == set(trace_io.IO_SIGNATURES)
     L = _lib.lib()
     assert all(hasattr(L, s) for s in gen.GEN_SIGNATURES)
+    assert all(hasattr(L, s) for s in trace_io.IO_SIGNATURES)
 
 
 def test_version_and_error_without_gpu():
