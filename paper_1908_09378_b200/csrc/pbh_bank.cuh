@@ -294,7 +294,10 @@ DEV void cta_sort(u32* K, u64* P, u32 n, u32* TK, u64* TP) {
   u32* dk = TK;
   u64* dp = TP;
   for (u32 wr = 128; wr < M; wr <<= 1) {
-    for (u32 o0 = tid * 4; o0 < M; o0 += 4 * NT) {
+    // each thread merges one contiguous range of M / NT outputs (one
+    // merge-path search per round)
+    const u32 per = M / NT;  // M >= 128 and NT <= 256: per >= 1 when M >= NT
+    for (u32 o0 = tid * per; o0 < M; o0 += per * NT) {
       const u32 base = (o0 / (2 * wr)) * 2 * wr;
       const u32 d = o0 - base;
       const u32* ak = sk + base;
@@ -310,17 +313,22 @@ DEV void cta_sort(u32* K, u64* P, u32 n, u32* TK, u64* TP) {
           hi = m;
       }
       u32 x = lo, y = d - lo;
-#pragma unroll
-      for (u32 v = 0; v < 4; ++v) {
-        const bool ta = x < wr && (y >= wr || less_pk(ap[x], ak[x], bp[y], bk[y]));
+      u64 xa = x < wr ? ap[x] : ~0ull, yb = y < wr ? bp[y] : ~0ull;
+      u32 xk = x < wr ? ak[x] : 0xffffffffu, yk = y < wr ? bk[y] : 0xffffffffu;
+      for (u32 v = 0; v < per; ++v) {
+        const bool ta = x < wr && (y >= wr || less_pk(xa, xk, yb, yk));
         if (ta) {
-          dk[o0 + v] = ak[x];
-          dp[o0 + v] = ap[x];
+          dk[o0 + v] = xk;
+          dp[o0 + v] = xa;
           ++x;
+          xa = x < wr ? ap[x] : ~0ull;
+          xk = x < wr ? ak[x] : 0xffffffffu;
         } else {
-          dk[o0 + v] = bk[y];
-          dp[o0 + v] = bp[y];
+          dk[o0 + v] = yk;
+          dp[o0 + v] = yb;
           ++y;
+          yb = y < wr ? bp[y] : ~0ull;
+          yk = y < wr ? bk[y] : 0xffffffffu;
         }
       }
     }
@@ -426,6 +434,18 @@ struct BankHeap {
     if (n == 0) return;
     long long t = clock64();
     to_cold();
+    if (__isShared(K) && n <= kBankQ) {
+      // stage the run in HBM (g_pk/g_pp hold kBankQ entries) so the merge
+      // into S_1 can stream through cp.async windows or run on the grid
+      for (u32 i = tid; i < n; i += B) {
+        hc.pk[i] = K[i];
+        hc.pp[i] = P[i];
+      }
+      __threadfence_block();
+      Bk::sync();
+      K = hc.pk;
+      P = hc.pp;
+    }
     hc.template push_down<true>(0, Run{K, P, n});
     pr(9, t);
     ++pushes;
@@ -442,7 +462,10 @@ struct BankHeap {
     const u32 n = qn;
     if (n == 0) return;
     long long t = clock64();
-    cta_sort<NW>(L.qk, L.qp, n, S.sk, S.sp);
+    // through bank_smem() (not the member references) so the inlined sort
+    // sees the shared address space and uses LDS/STS
+    auto& SS = bank_smem<NW, KI, VT, MW>();
+    cta_sort<NW>(SS.l0.qk, SS.l0.qp, n, SS.sk, SS.sp);
     pr(8, t);
     push_run(L.qk, L.qp, n);
     if (tid == 0) L.qn = 0;
@@ -1038,16 +1061,35 @@ __global__ void __launch_bounds__(32 * NW, 1)
       }
       // pass 1: validate (no mutation)
       bool bad_sort = false, bad_key = false, bad_dead = false, bad_inc = false;
-      for (u32 j = tid; j < n; j += B) {
-        const u32 k = vals[j];
-        if (check && j > 0 && vals[j - 1] >= k) bad_sort = true;
-        if (k >= universe) {
-          bad_key = true;
-          continue;
+      // 4 elements per thread per step: their loads are all in flight at once
+      for (u32 j0 = tid; j0 < n; j0 += 4 * B) {
+        u32 kk[4], kp[4];
+        ulonglong2 e[4];
+#pragma unroll
+        for (u32 t = 0; t < 4; ++t) {
+          const u32 j = j0 + t * B;
+          kk[t] = j < n ? vals[j] : 0;
+          kp[t] = j < n && j > 0 ? vals[j - 1] : 0;
         }
-        const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + k));
-        if (PBH_ST((u32)e.y) == PBH_ST_DEAD) bad_dead = true;
-        if (debug && PBH_ST((u32)e.y) == PBH_ST_LIVE && prios[j] > e.x) bad_inc = true;
+#pragma unroll
+        for (u32 t = 0; t < 4; ++t) {
+          const u32 j = j0 + t * B;
+          e[t] = j < n && kk[t] < universe
+                     ? __ldcg(reinterpret_cast<const ulonglong2*>(idx + kk[t]))
+                     : make_ulonglong2(0, 0);
+        }
+#pragma unroll
+        for (u32 t = 0; t < 4; ++t) {
+          const u32 j = j0 + t * B;
+          if (j >= n) continue;
+          if (check && j > 0 && kp[t] >= kk[t]) bad_sort = true;
+          if (kk[t] >= universe) {
+            bad_key = true;
+            continue;
+          }
+          if (PBH_ST((u32)e[t].y) == PBH_ST_DEAD) bad_dead = true;
+          if (debug && PBH_ST((u32)e[t].y) == PBH_ST_LIVE && prios[j] > e[t].x) bad_inc = true;
+        }
       }
       TPROF(6);
       const u32 bad = (u32)__syncthreads_or(bad_sort) | ((u32)__syncthreads_or(bad_key) << 1) |
@@ -1060,8 +1102,17 @@ __global__ void __launch_bounds__(32 * NW, 1)
       // pass 2: apply, one element per thread per pass
       TPROF(0);
       bool cold_fail = false;
+      u32 nx_u = 0;
+      u64 nx_c = 0;
+      ulonglong2 nx_e = make_ulonglong2(0, 0);
+      if (tid < n) {
+        nx_u = vals[tid];
+        nx_c = prios[tid];
+        nx_e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + nx_u));
+      }
       for (u32 base = 0; base < n; base += B) {
-        if (evict_due || qn > (u32)(kBankQ - B)) {
+        const bool cold_now = evict_due || qn > (u32)(kBankQ - B);
+        if (cold_now) {
           TPROF(1);
           BANK_TO_H();
           if (evict_due) H.evict();
@@ -1077,10 +1128,22 @@ __global__ void __launch_bounds__(32 * NW, 1)
         }
         const u32 j = base + tid;
         bool fresh = false, pushed = false;
+        // this pass's element came with the previous pass (prefetch below);
+        // a cold op just now (evict) may have moved its slot: re-read then
+        const u32 u = nx_u;
+        const u64 c = nx_c;
+        const ulonglong2 e = cold_now && j < n
+                                 ? __ldcg(reinterpret_cast<const ulonglong2*>(idx + u))
+                                 : nx_e;
+        {
+          const u32 jn = j + B;  // next pass (distinct keys: no conflict)
+          if (jn < n) {
+            nx_u = vals[jn];
+            nx_c = prios[jn];
+            nx_e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + nx_u));
+          }
+        }
         if (j < n) {
-          const u32 u = vals[j];
-          const u64 c = prios[j];
-          const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + u));
           const u32 st = (u32)e.y;
           fresh = PBH_ST(st) != PBH_ST_LIVE;
           if (fresh || c < e.x) {

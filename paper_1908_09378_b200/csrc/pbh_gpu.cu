@@ -436,6 +436,8 @@ pbh_status alloc_level(DevHeap& H, u32 i) {
 pbh_status alloc_scratch(DevHeap& H, u32 bc, u32 nt, cudaStream_t strm = 0) {
   pbh_status st;
   H.bc = bc;
+  // the banked engines stage push-buffer runs (kBankQ entries) in g_pk/g_pp
+  if (H.base1 == 4ull * kBankQ) bc = std::max<u32>(bc, kBankQ);
   if ((st = H.alloc((void**)&H.hd.g_bk, (u64)bc * 4))) return st;
   if ((st = H.alloc((void**)&H.hd.g_bp, (u64)bc * 8))) return st;
   if ((st = H.alloc((void**)&H.hd.g_pk, (u64)bc * 4))) return st;

@@ -1,3 +1,2 @@
-set -x
-timeout 1200 python tools/bench_suite.py thr > gpurun_out/suite_thr.json 2> gpurun_out/suite_thr.log
-tail -n 4 gpurun_out/suite_thr.log | cut -c1-400
+PBH_PROF=1 timeout 600 python tools/probe_trace.py c1 fill 2>&1 | grep -o '"us_per_op": [0-9.]*\|push_down [0-9]*\|sort [0-9]*'
+timeout 600 python -m pytest tests/test_heap_gpu.py -x -q 2>&1 | tail -1
