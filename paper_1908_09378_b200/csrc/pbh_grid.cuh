@@ -22,7 +22,7 @@
 namespace pbh_dev {
 
 constexpr u32 kGridTile = 2048;   // outputs per streamed tile
-constexpr u32 kGridMin = 16384;   // smallest merge worth a grid job
+constexpr u32 kGridMin = 2048;    // smallest merge worth a grid job (measured sweep 2K..16K: 2K best)
 constexpr u32 kStreamMin = 64;    // smallest merge streamed through the windows by one CTA
 
 // Job word + descriptor in HBM (one per heap handle).

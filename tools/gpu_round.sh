@@ -1,2 +1,4 @@
-PBH_PROF=1 timeout 600 python tools/probe_trace.py c1 fill 2>&1 | grep -o '"us_per_op": [0-9.]*\|push_down [0-9]*\|sort [0-9]*'
-timeout 600 python -m pytest tests/test_heap_gpu.py -x -q 2>&1 | tail -1
+set -x
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 2400 python tools/bench_suite.py c1 c3 c4 --c4-n 26 --c4-ds 32,1024,65536 > gpurun_out/suite.json 2> gpurun_out/suite.log
+tail -n 3 gpurun_out/pytest_gpu.log; cut -c1-300 gpurun_out/suite.log
