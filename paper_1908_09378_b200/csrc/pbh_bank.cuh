@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
         ee[t] = make_ulonglong2(~0ull, PBH_ST_DEAD);
         ob[t] = oe[t] = 0;
         if (te + B * t < rem) {
-          ee[t] = __ldcg(reinterpret_cast<const ulonglong2*>(idx + uu[t]));
+          ee[t] = __ldca(reinterpret_cast<const ulonglong2*>(idx + uu[t]));  // L1: sole writer is this CTA
           ob[t] = __ldg(off + uu[t]);
           oe[t] = __ldg(off + uu[t] + 1);
         }

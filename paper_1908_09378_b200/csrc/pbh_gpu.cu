@@ -275,6 +275,8 @@ struct BankCfg;
 template <>
 struct BankCfg<1> { static constexpr int KI = 32; };
 template <>
+struct BankCfg<2> { static constexpr int KI = 16; };
+template <>
 struct BankCfg<4> { static constexpr int KI = 8; };
 template <>
 struct BankCfg<8> { static constexpr int KI = 4; };
@@ -285,7 +287,8 @@ size_t bank_save_bytes() {
   return sizeof(BankL0<32 * NW, BankCfg<NW>::KI>);
 }
 size_t bank_save_bytes_nw(int nw) {
-  return nw == 1 ? bank_save_bytes<1>() : nw == 4 ? bank_save_bytes<4>() : bank_save_bytes<8>();
+  return nw == 1 ? bank_save_bytes<1>() : nw == 2 ? bank_save_bytes<2>()
+         : nw == 4 ? bank_save_bytes<4>() : bank_save_bytes<8>();
 }
 
 template <int NW>
@@ -333,6 +336,7 @@ cudaError_t launch_sssp_bank_nw(int nw, cudaStream_t st, u32 grid, pbh_heap_dev*
                                 void* save, u32 dag, u32 maxdeg, u32 d) {
   switch (nw) {
     case 1: return launch_sssp_bank<1>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
+    case 2: return launch_sssp_bank<2>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
     case 4: return launch_sssp_bank<4>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
     default: return launch_sssp_bank<8>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
   }
@@ -1184,7 +1188,7 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
   if (c->lane) {
     c->bank_nw = 4;
     if (const char* e = getenv("PBH_SSSP_NW")) c->bank_nw = atoi(e);
-    if (c->bank_nw != 1 && c->bank_nw != 4 && c->bank_nw != 8) c->bank_nw = 4;
+    if (c->bank_nw != 1 && c->bank_nw != 2 && c->bank_nw != 4 && c->bank_nw != 8) c->bank_nw = 4;
     c->cap0 = kBankC0 / 2;
     c->nt = 32 * c->bank_nw;
   } else if (c->fast) {
