@@ -166,6 +166,15 @@ pbh_status pbh_sssp_ctx_fetch(pbh_sssp_ctx* c, uint64_t source_slot, uint64_t* d
 pbh_status pbh_sssp_ctx_set_mode(pbh_sssp_ctx* c, int mode);
 pbh_status pbh_sssp_ctx_destroy(pbh_sssp_ctx* c);
 
+/* The multi-source batch of pbh_sssp_multi with the results gathered on
+ * devices[0] over NVLink (peer copies, no collective): dist_dev0 /
+ * parent_dev0 (may be NULL) are device pointers on devices[0] holding
+ * n_sources * V entries, source-major. device_ms = max over devices of the
+ * solve time. */
+pbh_status pbh_sssp_multi_device(const pbh_csr* g, const uint32_t* sources, uint64_t n_sources,
+                                 uint64_t d, const int* devices, int n_devices,
+                                 uint64_t* dist_dev0, uint32_t* parent_dev0, double* device_ms);
+
 /* bellman_ford (sssp.hpp:37, sssp.cpp:99-129) on the device: a frontier
  * label-correcting sweep (one cooperative grid, 64-bit atomicMin), the
  * baseline the bucket heap is compared with. Distances are

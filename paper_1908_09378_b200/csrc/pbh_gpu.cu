@@ -1548,6 +1548,55 @@ pbh_status pbh_host_unregister(void* ptr) {
   return PBH_OK;
 }
 
+pbh_status pbh_sssp_multi_device(const pbh_csr* g, const uint32_t* sources, uint64_t n_sources,
+                                 uint64_t d, const int* devices, int n_devices,
+                                 uint64_t* dist_dev0, uint32_t* parent_dev0, double* device_ms) {
+  if (!g || !sources || !dist_dev0 || n_devices <= 0 || n_sources == 0)
+    return set_err(PBH_PRECONDITION, "bad arguments");
+  const int dev0 = devices[0];
+  std::vector<pbh_status> res(n_devices, PBH_OK);
+  std::vector<std::string> msg(n_devices);
+  std::vector<double> ms(n_devices, 0.0);
+  std::vector<std::thread> th;
+  const u64 V = g->vertex_count;
+  const u64 per = (n_sources + n_devices - 1) / n_devices;
+  for (int r = 0; r < n_devices; ++r) {
+    const u64 b = std::min<u64>(n_sources, r * per), e = std::min<u64>(n_sources, b + per);
+    if (b >= e) continue;
+    th.emplace_back([&, r, b, e] {
+      pbh_sssp_ctx* c = nullptr;
+      pbh_status st = pbh_sssp_ctx_create(g, d, devices[r], e - b, &c);
+      if (!st) st = pbh_sssp_ctx_run(c, sources + b, e - b, 0, &ms[r]);
+      if (!st) {
+        // gather this shard's dist / parent rows into devices[0] over NVLink
+        if (devices[r] != dev0) {
+          int can = 0;
+          cudaDeviceCanAccessPeer(&can, devices[r], dev0);
+          if (can) {
+            cudaError_t pe = cudaDeviceEnablePeerAccess(dev0, 0);
+            if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+          }
+        }
+        cudaError_t ce = cudaMemcpyPeerAsync(dist_dev0 + b * V, dev0, c->d_dist, devices[r],
+                                             (e - b) * V * 8, c->stream);
+        if (ce == cudaSuccess && parent_dev0)
+          ce = cudaMemcpyPeerAsync(parent_dev0 + b * V, dev0, c->d_parent, devices[r],
+                                   (e - b) * V * 4, c->stream);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
+        if (ce != cudaSuccess) st = set_err(PBH_CUDA, std::string("peer gather: ") + cudaGetErrorString(ce));
+      }
+      if (c) pbh_sssp_ctx_destroy(c);
+      res[r] = st;
+      if (st) msg[r] = g_last_error;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int r = 0; r < n_devices; ++r)
+    if (res[r]) return set_err(res[r], msg[r]);
+  if (device_ms) *device_ms = *std::max_element(ms.begin(), ms.end());
+  return PBH_OK;
+}
+
 uint64_t pbh_distance_checksum(const uint64_t* dist, uint64_t n) {
   uint64_t h = 0xcbf29ce484222325ull;
   for (uint64_t i = 0; i < n; ++i)

@@ -235,6 +235,22 @@ def validate_parent_tree(g, source, dist, parent) -> str | None:
     return None
 
 
+def par_dijkstra_multi_device(g, sources, dist_dev0: int, parent_dev0: int = 0, d: int = 0,
+                              devices=(0,)) -> float:
+    """pbh_sssp_multi_device: results gathered on devices[0] over NVLink into
+    the device buffers at the given addresses (e.g. torch ``data_ptr()``).
+    Returns the max-over-devices solve time in ms."""
+    g = CsrGraph.of(g)
+    cs = g.c_struct()
+    src = np.ascontiguousarray(sources, dtype=np.uint32)
+    devs = (C.c_int * len(devices))(*devices)
+    ms = C.c_double()
+    raise_for(_lib.lib().pbh_sssp_multi_device(
+        C.byref(cs), src.ctypes.data_as(_lib.U32P), len(src), d, devs, len(devices),
+        C.c_void_p(dist_dev0), C.c_void_p(parent_dev0 or None), C.byref(ms)))
+    return ms.value
+
+
 def pin(*arrays):
     """Page-lock numpy arrays for fast host<->device copies (pbh_host_register)."""
     for a in arrays:

@@ -1,1 +1,1 @@
-for nw in 2 4 8; do echo "nw=$nw"; PBH_SSSP_NW=$nw timeout 600 python -m pytest tests/test_sssp_gpu.py -x -q 2>&1 | tail -1; PBH_SSSP_NW=$nw timeout 300 python tools/probe.py band_small band band64 grid_small 2>&1 | grep -o '"name": "[a-zA-Z0-9_^]*"\|"ns_per_round": [0-9.]*'; done
+timeout 600 python -m pytest tests/test_multi_gpu.py tests/test_trace_io.py tests/test_bf_gpu.py -x -q 2>&1 | tail -15
