@@ -45,6 +45,16 @@ void pbh_gen_sweep_prefill(uint64_t n, uint64_t seed, uint64_t* prios_now);
 void pbh_gen_sweep_batches(uint64_t n, uint64_t d, uint64_t n_batches, uint64_t seed,
                            uint64_t* prios_now, uint32_t* values, uint64_t* priorities);
 
+/* Device versions: the same C2 grid / C3 band built
+ * directly in device memory (pointers on `device`), bit-identical to the host
+ * generators; one CTA replays std::mt19937_64 twist by twist. Return a
+ * pbh_status (0 = ok). The CSR may then be passed to pbh_sssp_ctx_create as
+ * device pointers (copied device-to-device). */
+int pbh_gen_grid_device(uint32_t rows, uint32_t cols, uint64_t seed, int device,
+                        uint64_t* offsets, uint32_t* targets, uint32_t* weights);
+int pbh_gen_band_device(uint32_t v, uint32_t degree, uint64_t seed, int device,
+                        uint64_t* offsets, uint32_t* targets, uint32_t* weights);
+
 #ifdef __cplusplus
 }
 #endif

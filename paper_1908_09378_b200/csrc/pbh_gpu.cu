@@ -19,6 +19,8 @@
 #include "pbh_bank.cuh"
 #include "pbh_bf.cuh"
 #include "pbh_multi.cuh"
+#include "pbh_gen_gpu.cuh"
+#include "../../include/pbh_gen.h"
 
 using namespace pbh_dev;
 
@@ -1161,9 +1163,10 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
   if ((st = ctx_alloc(c, (void**)&c->d_off, ((u64)c->V + 1) * 8))) return fail(st);
   if ((st = ctx_alloc(c, (void**)&c->d_tgt, c->E * 4))) return fail(st);
   if ((st = ctx_alloc(c, (void**)&c->d_w, c->E * 4))) return fail(st);
-  if (cudaMemcpyAsync(c->d_off, g->offsets, ((u64)c->V + 1) * 8, cudaMemcpyHostToDevice, c->stream) ||
-      (c->E && cudaMemcpyAsync(c->d_tgt, g->targets, c->E * 4, cudaMemcpyHostToDevice, c->stream)) ||
-      (c->E && cudaMemcpyAsync(c->d_w, g->weights, c->E * 4, cudaMemcpyHostToDevice, c->stream)))
+  // host or device CSR arrays (unified addressing: cudaMemcpyDefault)
+  if (cudaMemcpyAsync(c->d_off, g->offsets, ((u64)c->V + 1) * 8, cudaMemcpyDefault, c->stream) ||
+      (c->E && cudaMemcpyAsync(c->d_tgt, g->targets, c->E * 4, cudaMemcpyDefault, c->stream)) ||
+      (c->E && cudaMemcpyAsync(c->d_w, g->weights, c->E * 4, cudaMemcpyDefault, c->stream)))
     return fail(set_err(PBH_CUDA, "CSR upload failed"));
   // max out-degree on the device (graphs.cpp:47-53)
   unsigned long long* d_md = nullptr;
@@ -1534,6 +1537,58 @@ pbh_status pbh_bellman_ford(const pbh_csr* g, uint32_t source, int device, uint6
   if (edges_scanned) *edges_scanned = hs.relaxed;
   if (device_ms) *device_ms = ms;
   return fin(PBH_OK);
+}
+
+namespace {
+
+// kind 0 = grid (rows x cols), 1 = band (V, degree); device output arrays.
+pbh_status gen_device(u32 kind, u32 rows, u32 cols, u32 V, u32 degree, u64 seed, int device,
+                      u64* off, u32* tgt, u32* w) {
+  CK(cudaSetDevice(device));
+  // std::mt19937_64 seeding (the state the first twist starts from)
+  u64 mt[kMtN];
+  mt[0] = seed;
+  for (int i = 1; i < kMtN; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (u64)i;
+  u64* d_mt = nullptr;
+  CK(cudaMalloc(&d_mt, sizeof mt));
+  cudaStream_t st = nullptr;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  cudaMemcpyAsync(d_mt, mt, sizeof mt, cudaMemcpyHostToDevice, st);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  k_gen_structure<<<sms * 8, 256, 0, st>>>(kind, rows, cols, V, degree, off, tgt, w);
+  GenMap map{};
+  map.kind = kind;
+  map.V = V;
+  map.degree = degree;
+  map.w = w;
+  if (kind == 0) {
+    map.n_draws = pbh_gen_grid_edges(rows, cols);
+  } else {
+    map.n_draws = V == 0 ? 0 : (u64)(V - 1) * (degree - 1) + degree;
+  }
+  k_gen_weights<<<1, 320, 0, st>>>(d_mt, map);
+  g_launches += 2;
+  cudaError_t e = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  cudaFree(d_mt);
+  if (e != cudaSuccess) return set_err(PBH_CUDA, std::string("device generator: ") + cudaGetErrorString(e));
+  return PBH_OK;
+}
+
+}  // namespace
+
+int pbh_gen_grid_device(uint32_t rows, uint32_t cols, uint64_t seed, int device,
+                               uint64_t* offsets, uint32_t* targets, uint32_t* weights) {
+  if (!rows || !cols || !offsets || !targets || !weights) return set_err(PBH_PRECONDITION, "bad arguments");
+  return gen_device(0, rows, cols, rows * cols, 0, seed, device, offsets, targets, weights);
+}
+
+int pbh_gen_band_device(uint32_t v, uint32_t degree, uint64_t seed, int device,
+                               uint64_t* offsets, uint32_t* targets, uint32_t* weights) {
+  if (!v || !degree || degree >= v || !offsets || !targets || !weights)
+    return set_err(PBH_PRECONDITION, "bad arguments");
+  return gen_device(1, 0, 0, v, degree, seed, device, offsets, targets, weights);
 }
 
 pbh_status pbh_host_register(void* ptr, uint64_t bytes) {

@@ -134,7 +134,8 @@ class SsspContext:
 
     def __init__(self, g, d: int = 0, device: int = 0, max_sources: int = 1,
                  mode: str = "exact"):
-        self.g = CsrGraph.of(g)
+        # a DeviceCsr (gen.band_device / grid_device) is copied device-to-device
+        self.g = g if hasattr(g, "data_ptr") or type(g).__name__ == "DeviceCsr" else CsrGraph.of(g)
         cs = self.g.c_struct()
         h = C.c_void_p()
         raise_for(_lib.lib().pbh_sssp_ctx_create(C.byref(cs), d, device, max_sources, C.byref(h)))

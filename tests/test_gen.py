@@ -1,6 +1,7 @@
 """The product's workload generators (include/pbh_gen.h, C++) must agree draw
 for draw with the oracle's independent restatement (oracle/pbh_oracle.c)."""
 import numpy as np
+import pytest
 
 
 def test_grid_matches_oracle(O):
@@ -43,3 +44,39 @@ def test_sweep_batches_are_strict_decreases():
         vb = v[b * 32:(b + 1) * 32]
         assert np.all(np.diff(vb.astype(np.int64)) > 0)
     assert np.all(pr <= before)
+
+
+# ---- device generators: bit-identical to the host ones
+@pytest.mark.gpu
+@pytest.mark.parametrize("v,deg", [(4096, 64), (1 << 16, 256), (300, 1), (1000, 999)])
+def test_band_device_matches_host(v, deg):
+    from paper_1908_09378_b200 import gen
+    want = gen.band(v, deg, 2)
+    got = gen.band_device(v, deg, 2).to_host()
+    assert np.array_equal(got.offsets, want.offsets)
+    assert np.array_equal(got.targets, want.targets)
+    assert np.array_equal(got.weights, want.weights)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("r,c", [(64, 64), (1, 50), (37, 1), (333, 517)])
+def test_grid_device_matches_host(r, c):
+    from paper_1908_09378_b200 import gen
+    want = gen.grid(r, c, 1)
+    got = gen.grid_device(r, c, 1).to_host()
+    assert np.array_equal(got.offsets, want.offsets)
+    assert np.array_equal(got.targets, want.targets)
+    assert np.array_equal(got.weights, want.weights)
+
+
+@pytest.mark.gpu
+def test_sssp_on_device_generated_graph():
+    import paper_1908_09378_b200 as P
+    from paper_1908_09378_b200 import gen
+    gd = gen.band_device(8192, 64, 2)
+    ctx = P.SsspContext(gd, max_sources=1)
+    ctx.run([0])
+    r = ctx.fetch(0, settled=False)
+    ctx.close()
+    host = P.par_dijkstra(gen.band(8192, 64, 2), 0)
+    assert np.array_equal(r.dist, host.dist)
