@@ -567,7 +567,8 @@ template <int NW, int KI, int VT>
 __global__ void __launch_bounds__(32 * NW, 1)
     k_sssp_bank(pbh_heap_dev* heaps, const u64* __restrict__ off, const u32* __restrict__ tgt,
                 const u32* __restrict__ wt, u32 V, const u32* sources, u64* dist, u32* settled,
-                SsspState* sst, BankL0<32 * NW, KI>* save, u32 dag_mode, u32 max_deg, u32 d) {
+                SsspState* sst, BankL0<32 * NW, KI>* save, u32 dag_mode, u32 max_deg, u32 d,
+                unsigned long long* prof) {
   using BH = BankHeap<NW, KI, VT>;
   using HC = typename BH::HC;
   using Bk = Blk<BH::B>;
@@ -668,6 +669,15 @@ __global__ void __launch_bounds__(32 * NW, 1)
   bool nx = false;            // the next extraction is known (cur)
   BankOffer cur{};
   bool fail_bad = false, fail_ovf = false;
+  // PBH_PROF: thread-0 cycle breakdown of a round (prof[0..7])
+  u64 pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long pt = clock64();
+#define SPROF(i)                          \
+  if (prof) {                             \
+    const long long t1_ = clock64();      \
+    pc[i] += (u64)(t1_ - pt);             \
+    pt = t1_;                             \
+  }
   u32 fail_v = 0;
   while (live > 0) {
     if (!grow_ok || (u64)qn + deep_n > grow_at) {
@@ -696,6 +706,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
       }
     }
     nx = false;
+    SPROF(0);
     const u64 p = cur.p;
     const u32 v = cur.k;
     if (cur.slot % B == tid) {
@@ -735,6 +746,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
         }
       }
       u32 uu[PE], ww[PE];
+      SPROF(1);
       if (hit && done == 0) {
         cp_async_wait_all();
 #pragma unroll
@@ -752,6 +764,13 @@ __global__ void __launch_bounds__(32 * NW, 1)
       }
       ulonglong2 ee[PE];
       u64 ob[PE], oe[PE];
+      if (prof) {  // make the row load visible in its own bucket
+        u32 sink = 0;
+#pragma unroll
+        for (u32 t = 0; t < PE; ++t) sink += uu[t];
+        if (sink == 0xfffffffeu) pc[7] += 1;
+      }
+      SPROF(2);
 #pragma unroll
       for (u32 t = 0; t < PE; ++t) {
         ee[t] = make_ulonglong2(~0ull, PBH_ST_DEAD);
@@ -767,6 +786,13 @@ __global__ void __launch_bounds__(32 * NW, 1)
       if (rescan_due) bank_rescan<B, KI>(L, tid, occm, lhas, lmin_p, lmin_k, lmin_s);
       rescan_due = false;
       // ---- candidates, applied by the relaxing thread
+      if (prof) {
+        u32 sink = 0;
+#pragma unroll
+        for (u32 t = 0; t < PE; ++t) sink += (u32)ee[t].y;
+        if (sink == 0xfffffffeu) pc[7] += 1;
+      }
+      SPROF(3);
       u32 fresh = 0, nimp = 0, nq = 0;
       bool ovf = false, bad = false;
       bool ch = false;
@@ -835,6 +861,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
         e.parent = v;
         reinterpret_cast<ulonglong2*>(idx)[u] = *reinterpret_cast<const ulonglong2*>(&e);
       }
+      SPROF(4);
       // ---- exchange: this thread offers min(bank minimum, best candidate)
       bool oh = lhas;
       u64 op = lmin_p;
@@ -869,6 +896,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
         fail_v = v;
         break;
       }
+      SPROF(5);
       if (last && r.has) {
         // the next extraction: load its row's first pass now
         nx = true;
@@ -884,11 +912,15 @@ __global__ void __launch_bounds__(32 * NW, 1)
         cp_async_commit();
       }
     }
+    SPROF(6);
     if (cold_fail || fail_bad || fail_ovf) break;
     // bulk_update batches of <= d (sssp.cpp:59-64)
     if (n_imp) ops += n_imp <= d ? 1u : (n_imp + d - 1) / d;
   }
   cp_async_wait_all();
+#undef SPROF
+  if (prof && (threadIdx.x & 31) == 0 && blockIdx.x == 0)
+    for (int i = 0; i < 8; ++i) atomicAdd(prof + (threadIdx.x >> 5) * 8 + i, (unsigned long long)pc[i]);
   BANK_TO_H();
 #undef BANK_TO_H
 #undef BANK_FROM_H

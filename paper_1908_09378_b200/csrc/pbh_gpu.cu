@@ -306,8 +306,19 @@ cudaError_t launch_sssp_bank(cudaStream_t st, u32 grid, pbh_heap_dev* heaps, con
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  static unsigned long long* prof = nullptr;
+  if (getenv("PBH_PHASES") && !prof && cudaMalloc(&prof, 64 * 8) == cudaSuccess) cudaMemset(prof, 0, 64 * 8);
   fn<<<grid, 32 * NW, smem, st>>>(heaps, off, tgt, w, V, src, dist, settled, sst,
-                                  reinterpret_cast<BankL0<32 * NW, KI>*>(save), dag, maxdeg, d);
+                                  reinterpret_cast<BankL0<32 * NW, KI>*>(save), dag, maxdeg, d,
+                                  prof);
+  if (prof) {
+    unsigned long long pc[64];
+    cudaMemcpy(pc, prof, 64 * 8, cudaMemcpyDeviceToHost);
+    cudaMemset(prof, 0, 64 * 8);
+    for (int w = 0; w < NW; ++w)
+      fprintf(stderr, "bank phases warp %d (cycles, source 0): top %llu pre-row %llu row %llu gather %llu apply %llu exchange %llu tail %llu\n",
+              w, pc[w * 8 + 0], pc[w * 8 + 1], pc[w * 8 + 2], pc[w * 8 + 3], pc[w * 8 + 4], pc[w * 8 + 5], pc[w * 8 + 6]);
+  }
   g_launches++;
   return cudaGetLastError();
 }
