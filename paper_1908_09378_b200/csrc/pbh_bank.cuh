@@ -137,12 +137,17 @@ DEV void bank_rescan(const BankL0<B, KI, MW>& L, u32 tid, u32 occm, bool& lhas, 
 // and row, and the sums of the counters. One barrier. Counters are packed
 // 9 bits each (every one is <= 256 per pass): c0 = fresh | nimp << 9 |
 // ovf << 18, c1 = nq | evict << 9 | bad << 18 (the last two per-thread flags).
+__device__ unsigned long long g_xprof[8];  // PBH_PHASES: exchange breakdown (thread 0, block 0)
+
 template <int NW, int KI, int VT, bool MW = false>
 DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u32 deg, u32 c0,
                             u32 c1, u64 t = ~0ull) {
   BankSmem<NW, KI, VT, MW>& S = bank_smem<NW, KI, VT, MW>();
   const u32 tid = threadIdx.x;
   const u32 lane = tid & 31, w = tid >> 5;
+#ifdef PBH_XPROF
+  const long long xa = clock64();
+#endif
   bool h = has;
   u64 wp = p;
   u32 wk = k;
@@ -183,7 +188,13 @@ DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u
     r.flags = ((s1 >> 9) & 511u ? 1u : 0u) | ((s1 >> 18) & 511u ? 2u : 0u) | ((s0 >> 18) & 511u ? 4u : 0u);
     return r;
   } else {
+#ifdef PBH_XPROF
+    const long long xb = clock64();
+#endif
     __syncthreads();
+#ifdef PBH_XPROF
+    const long long xc = clock64();
+#endif
     // tree argmin over the NW warp winners (index only), then one read
     u32 bi = 0;
     bool bh = S.ex[par][0].has;
@@ -218,6 +229,15 @@ DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u
     r.nimp = (t0 >> 9) & 511u;
     r.nq = t1 & 511u;
     r.flags = ((t1 >> 9) & 511u ? 1u : 0u) | ((t1 >> 18) & 511u ? 2u : 0u) | ((t0 >> 18) & 511u ? 4u : 0u);
+#ifdef PBH_XPROF
+    if (blockIdx.x == 0 && (tid & 31) == 0) {
+      const long long xd = clock64();
+      atomicAdd(&g_xprof[0], (unsigned long long)(xb - xa));
+      atomicAdd(&g_xprof[1], (unsigned long long)(xc - xb));
+      atomicAdd(&g_xprof[2], (unsigned long long)(xd - xc));
+      atomicAdd(&g_xprof[3], 1ull);
+    }
+#endif
     return r;
   }
 }
@@ -669,8 +689,10 @@ __global__ void __launch_bounds__(32 * NW, 1)
   bool nx = false;            // the next extraction is known (cur)
   BankOffer cur{};
   bool fail_bad = false, fail_ovf = false;
-  // PBH_PROF: thread-0 cycle breakdown of a round (prof[0..7])
+  // round-phase breakdown per warp (build with -DPBH_PROF_BUILD, run with
+  // PBH_PHASES=1); compiled out otherwise (it costs ~7 % of a round)
   u64 pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#ifdef PBH_PROF_BUILD
   long long pt = clock64();
 #define SPROF(i)                          \
   if (prof) {                             \
@@ -678,6 +700,10 @@ __global__ void __launch_bounds__(32 * NW, 1)
     pc[i] += (u64)(t1_ - pt);             \
     pt = t1_;                             \
   }
+#else
+#define SPROF(i)
+  prof = nullptr;
+#endif
   u32 fail_v = 0;
   while (live > 0) {
     if (!grow_ok || (u64)qn + deep_n > grow_at) {
@@ -764,12 +790,14 @@ __global__ void __launch_bounds__(32 * NW, 1)
       }
       ulonglong2 ee[PE];
       u64 ob[PE], oe[PE];
+#ifdef PBH_PROF_BUILD
       if (prof) {  // make the row load visible in its own bucket
         u32 sink = 0;
 #pragma unroll
         for (u32 t = 0; t < PE; ++t) sink += uu[t];
         if (sink == 0xfffffffeu) pc[7] += 1;
       }
+#endif
       SPROF(2);
 #pragma unroll
       for (u32 t = 0; t < PE; ++t) {
@@ -786,12 +814,14 @@ __global__ void __launch_bounds__(32 * NW, 1)
       if (rescan_due) bank_rescan<B, KI>(L, tid, occm, lhas, lmin_p, lmin_k, lmin_s);
       rescan_due = false;
       // ---- candidates, applied by the relaxing thread
+#ifdef PBH_PROF_BUILD
       if (prof) {
         u32 sink = 0;
 #pragma unroll
         for (u32 t = 0; t < PE; ++t) sink += (u32)ee[t].y;
         if (sink == 0xfffffffeu) pc[7] += 1;
       }
+#endif
       SPROF(3);
       u32 fresh = 0, nimp = 0, nq = 0;
       bool ovf = false, bad = false;

@@ -315,6 +315,12 @@ cudaError_t launch_sssp_bank(cudaStream_t st, u32 grid, pbh_heap_dev* heaps, con
     unsigned long long pc[64];
     cudaMemcpy(pc, prof, 64 * 8, cudaMemcpyDeviceToHost);
     cudaMemset(prof, 0, 64 * 8);
+#ifdef PBH_XPROF
+    unsigned long long xp[8];
+    cudaMemcpyFromSymbol(xp, g_xprof, sizeof xp);
+    if (xp[3]) fprintf(stderr, "exchange per call (warp leaders, block 0): reduce %.0f barrier %.0f combine %.0f (n=%llu)\n",
+                       (double)xp[0] / xp[3], (double)xp[1] / xp[3], (double)xp[2] / xp[3], xp[3]);
+#endif
     for (int w = 0; w < NW; ++w)
       fprintf(stderr, "bank phases warp %d (cycles, source 0): top %llu pre-row %llu row %llu gather %llu apply %llu exchange %llu tail %llu\n",
               w, pc[w * 8 + 0], pc[w * 8 + 1], pc[w * 8 + 2], pc[w * 8 + 3], pc[w * 8 + 4], pc[w * 8 + 5], pc[w * 8 + 6]);
