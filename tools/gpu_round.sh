@@ -1,2 +1,3 @@
-timeout 600 python -m pytest tests/test_sssp_gpu.py -x -q 2>&1 | tail -1
-timeout 300 python tools/probe.py band_small band band64 grid_small 2>&1 | grep -o '"name": "[a-zA-Z0-9_^]*"\|"ns_per_round": [0-9.]*'
+timeout 900 compute-sanitizer --tool racecheck --print-limit 40 python tools/sanitize.py sssp > gpurun_out/race.log 2>&1
+grep -c "Race reported" gpurun_out/race.log
+grep -A1 "Race reported" gpurun_out/race.log | grep -o "at [^ ]*+0x[0-9a-f]* in [a-z_.]*:[0-9]*" | sort | uniq -c | sort -rn | head -20
