@@ -242,133 +242,6 @@ DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u
   }
 }
 
-// Sort n <= kBankQ entries (K, P) in shared memory by (p, k) with the whole
-// CTA: the warps sort runs of 128 in registers (4 per lane, element
-// r*32 + lane; bitonic network, shuffles below stride 32), then merge-path
-// rounds (4 outputs per thread per step) double the run width, ping-ponging
-// through (TK, TP). Slots n.. of the padded width are (~0, ~0): they sort last.
-template <int NW>
-DEV void cta_sort(u32* K, u64* P, u32 n, u32* TK, u64* TP) {
-  constexpr u32 NT = 32 * NW;
-  const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  u32 M = 128;
-  while (M < n) M <<= 1;
-  for (u32 run = w; run * 128 < M; run += NW) {
-    u64 p[4];
-    u32 k[4];
-#pragma unroll
-    for (u32 r = 0; r < 4; ++r) {
-      const u32 i = run * 128 + r * 32 + lane;
-      p[r] = i < n ? P[i] : ~0ull;
-      k[r] = i < n ? K[i] : 0xffffffffu;
-    }
-#pragma unroll
-    for (u32 size = 2; size <= 128; size <<= 1) {
-#pragma unroll
-      for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
-        if (stride >= 32) {
-          const u32 rs = stride / 32;
-#pragma unroll
-          for (u32 r = 0; r < 4; ++r) {
-            if (r & rs) continue;
-            const u32 i = r * 32 + lane;  // lower element of the pair
-            const bool up = (i & size) == 0;
-            const bool gt = less_pk(p[r | rs], k[r | rs], p[r], k[r]);
-            if (gt == up) {
-              const u64 tp = p[r];
-              p[r] = p[r | rs];
-              p[r | rs] = tp;
-              const u32 tk = k[r];
-              k[r] = k[r | rs];
-              k[r | rs] = tk;
-            }
-          }
-        } else {
-#pragma unroll
-          for (u32 r = 0; r < 4; ++r) {
-            const u32 i = r * 32 + lane;
-            const u32 ohi = __shfl_xor_sync(0xffffffffu, (u32)(p[r] >> 32), stride);
-            const u32 olo = __shfl_xor_sync(0xffffffffu, (u32)p[r], stride);
-            const u32 ok = __shfl_xor_sync(0xffffffffu, k[r], stride);
-            const u64 op = ((u64)ohi << 32) | olo;
-            const bool up = (i & size) == 0;
-            const bool lower = (lane & stride) == 0;
-            const bool other_less = less_pk(op, ok, p[r], k[r]);
-            if (lower == up ? other_less : !other_less) {
-              p[r] = op;
-              k[r] = ok;
-            }
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (u32 r = 0; r < 4; ++r) {
-      K[run * 128 + r * 32 + lane] = k[r];
-      P[run * 128 + r * 32 + lane] = p[r];
-    }
-  }
-  __syncthreads();
-  u32* sk = K;
-  u64* sp = P;
-  u32* dk = TK;
-  u64* dp = TP;
-  for (u32 wr = 128; wr < M; wr <<= 1) {
-    // each thread merges one contiguous range of M / NT outputs (one
-    // merge-path search per round)
-    const u32 per = M / NT;  // M >= 128 and NT <= 256: per >= 1 when M >= NT
-    for (u32 o0 = tid * per; o0 < M; o0 += per * NT) {
-      const u32 base = (o0 / (2 * wr)) * 2 * wr;
-      const u32 d = o0 - base;
-      const u32* ak = sk + base;
-      const u64* ap = sp + base;
-      const u32* bk = sk + base + wr;
-      const u64* bp = sp + base + wr;
-      u32 lo = d > wr ? d - wr : 0, hi = d < wr ? d : wr;
-      while (lo < hi) {
-        const u32 m = (lo + hi) >> 1;
-        if (less_pk(ap[m], ak[m], bp[d - 1 - m], bk[d - 1 - m]))
-          lo = m + 1;
-        else
-          hi = m;
-      }
-      u32 x = lo, y = d - lo;
-      u64 xa = x < wr ? ap[x] : ~0ull, yb = y < wr ? bp[y] : ~0ull;
-      u32 xk = x < wr ? ak[x] : 0xffffffffu, yk = y < wr ? bk[y] : 0xffffffffu;
-      for (u32 v = 0; v < per; ++v) {
-        const bool ta = x < wr && (y >= wr || less_pk(xa, xk, yb, yk));
-        if (ta) {
-          dk[o0 + v] = xk;
-          dp[o0 + v] = xa;
-          ++x;
-          xa = x < wr ? ap[x] : ~0ull;
-          xk = x < wr ? ak[x] : 0xffffffffu;
-        } else {
-          dk[o0 + v] = yk;
-          dp[o0 + v] = yb;
-          ++y;
-          yb = y < wr ? bp[y] : ~0ull;
-          yk = y < wr ? bk[y] : 0xffffffffu;
-        }
-      }
-    }
-    __syncthreads();
-    u32* t1 = sk;
-    sk = dk;
-    dk = t1;
-    u64* t2 = sp;
-    sp = dp;
-    dp = t2;
-  }
-  if (sk != K) {
-    for (u32 i = tid; i < n; i += NT) {
-      K[i] = sk[i];
-      P[i] = sp[i];
-    }
-    __syncthreads();
-  }
-}
-
 template <int NW, int KI, int VT, bool MW = false>
 struct BankHeap {
   static constexpr int B = 32 * NW;
@@ -1005,7 +878,7 @@ template <int NW, int KI, int VT>
 __global__ void __launch_bounds__(32 * NW, 1)
     k_trace_bank(pbh_heap_dev* g, pbh_trace_dev tr, u64 op_begin, u64 op_end, u32* out_v,
                  u64* out_p, pbh_kstatus* ks, BankL0<32 * NW, KI>* save, u32 allow_internal,
-                 GridJob* gj, u32 grid_min, unsigned long long* prof) {
+                 GridJob* gj, u32 grid_min, unsigned long long* prof, BatchJob* bj) {
   using BH = BankHeap<NW, KI, VT>;
   using HC = typename BH::HC;
   using Bk = Blk<BH::B>;
@@ -1121,10 +994,47 @@ __global__ void __launch_bounds__(32 * NW, 1)
         hc.fail(PBH_ERR_NEED_GROW, Lnl);
         break;
       }
+      // a large batch is validated and classified by the whole grid: only
+      // the elements that touch level 0 stay with this CTA (list `lst`)
+      const bool big = bj != nullptr && gridDim.x > 1 && n >= kBigBatch;
+      u32 m_apply = n, stg_n = 0;
+      const u32* lst = nullptr;
+      if (big) {
+        if (tid == 0) {
+          bj->vals = vals;
+          bj->prios = prios;
+          bj->idx = idx;
+          bj->universe = universe;
+          bj->spl_p = L.spl_p;
+          bj->spl_k = L.spl_k;
+          bj->spl_inf = L.spl_inf;
+          bj->n = n;
+          bj->check = check ? 1u : 0u;
+          bj->debug = debug ? 1u : 0u;
+          bj->c0 = C0;
+          bj->stg_n = bj->ll_n = bj->fresh = bj->errs = 0;
+          T.g.job.ext = bj;
+        }
+        __threadfence();
+        Bk::sync();
+        grid_run<B>(gj, gridDim.x, 2, Run{}, Run{}, 0, Sink{}, 0, T.g, T.g.scr);
+        const u32 errs = *(volatile u32*)&bj->errs;
+        if (errs) {
+          hc.fail(errs & 1 ? PBH_ERR_UNSORTED : errs & 2 ? PBH_ERR_KEY_RANGE
+                  : errs & 4 ? PBH_ERR_REINSERT : PBH_ERR_INCREASE);
+          break;
+        }
+        grid_run<B>(gj, gridDim.x, 3, Run{}, Run{}, 0, Sink{}, 0, T.g, T.g.scr);
+        m_apply = *(volatile u32*)&bj->ll_n;
+        stg_n = *(volatile u32*)&bj->stg_n;
+        live += *(volatile u32*)&bj->fresh;
+        lst = bj->ll;
+        TPROF(6);
+      }
       // pass 1: validate (no mutation)
       bool bad_sort = false, bad_key = false, bad_dead = false, bad_inc = false;
       // 4 elements per thread per step: their loads are all in flight at once
-      for (u32 j0 = tid; j0 < n; j0 += 4 * B) {
+      for (u32 j0 = tid; !big && j0 < n; j0 += 4 * B) {
         u32 kk[4], kp[4];
         ulonglong2 e[4];
 #pragma unroll
@@ -1153,7 +1063,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
           if (debug && PBH_ST((u32)e[t].y) == PBH_ST_LIVE && prios[j] > e[t].x) bad_inc = true;
         }
       }
-      TPROF(6);
+      if (!big) TPROF(6);
       const u32 bad = (u32)__syncthreads_or(bad_sort) | ((u32)__syncthreads_or(bad_key) << 1) |
                       ((u32)__syncthreads_or(bad_dead) << 2) | ((u32)__syncthreads_or(bad_inc) << 3);
       if (bad) {
@@ -1167,12 +1077,13 @@ __global__ void __launch_bounds__(32 * NW, 1)
       u32 nx_u = 0;
       u64 nx_c = 0;
       ulonglong2 nx_e = make_ulonglong2(0, 0);
-      if (tid < n) {
-        nx_u = vals[tid];
-        nx_c = prios[tid];
+      if (tid < m_apply) {
+        const u32 jj = lst ? lst[tid] : tid;
+        nx_u = vals[jj];
+        nx_c = prios[jj];
         nx_e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + nx_u));
       }
-      for (u32 base = 0; base < n; base += B) {
+      for (u32 base = 0; base < m_apply; base += B) {
         const bool cold_now = evict_due || qn > (u32)(kBankQ - B);
         if (cold_now) {
           TPROF(1);
@@ -1194,18 +1105,19 @@ __global__ void __launch_bounds__(32 * NW, 1)
         // a cold op just now (evict) may have moved its slot: re-read then
         const u32 u = nx_u;
         const u64 c = nx_c;
-        const ulonglong2 e = cold_now && j < n
+        const ulonglong2 e = cold_now && j < m_apply
                                  ? __ldcg(reinterpret_cast<const ulonglong2*>(idx + u))
                                  : nx_e;
         {
           const u32 jn = j + B;  // next pass (distinct keys: no conflict)
-          if (jn < n) {
-            nx_u = vals[jn];
-            nx_c = prios[jn];
+          if (jn < m_apply) {
+            const u32 jj = lst ? lst[jn] : jn;
+            nx_u = vals[jj];
+            nx_c = prios[jj];
             nx_e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + nx_u));
           }
         }
-        if (j < n) {
+        if (j < m_apply) {
           const u32 st = (u32)e.y;
           fresh = PBH_ST(st) != PBH_ST_LIVE;
           if (fresh || c < e.x) {
@@ -1252,8 +1164,36 @@ __global__ void __launch_bounds__(32 * NW, 1)
         par ^= 1;
       }
       if (cold_fail) break;
-      if (tid == 0) sm.touches[0] += 2ull * n;
       TPROF(1);
+      if (big && stg_n) {
+        // the HBM-bound part of the batch: grid sort (chunks, then merge
+        // passes), one push_down of the sorted run into S_1
+        if (tid == 0) {
+          bj->sort_n = stg_n;
+          bj->src = 0;
+        }
+        __threadfence();
+        Bk::sync();
+        grid_run<B>(gj, gridDim.x, 4, Run{}, Run{}, 0, Sink{}, 0, T.g, T.g.scr);
+        u32 src = 0;
+        for (u32 w = kSortChunk; w < stg_n; w <<= 1) {
+          if (tid == 0) {
+            bj->width = w;
+            bj->src = src;
+          }
+          __threadfence();
+          Bk::sync();
+          grid_run<B>(gj, gridDim.x, 5, Run{}, Run{}, 0, Sink{}, 0, T.g, T.g.scr);
+          src ^= 1;
+        }
+        TPROF(8 - 1);
+        BANK_TO_H();
+        H.push_run(bj->sk[src], bj->sp[src], stg_n);
+        BANK_FROM_H();
+        if (hc.failed()) break;
+        TPROF(2);
+      }
+      if (tid == 0) sm.touches[0] += 2ull * n;
     } else if (kind == 'E' || (kind == kOpFind && allow_internal)) {
       // ------------------------------------------------ extract_min / find_min
       if (live <= 0) {

@@ -184,7 +184,8 @@ using TraceSmem = TraceBankSmem<kTraceNW, kTraceKI, VT>;
 
 cudaError_t launch_trace_bank(cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr, u64 b, u64 e,
                               u32* ov, u64* op, pbh_kstatus* ks, TraceImage* save, u32 internal,
-                              GridJob* gj, u32 grid_min, unsigned long long* prof) {
+                              GridJob* gj, u32 grid_min, unsigned long long* prof,
+                              BatchJob* bj) {
   auto fn = k_trace_bank<kTraceNW, kTraceKI, VT>;
   const int smem = (int)sizeof(TraceSmem);
   static int G = 0;
@@ -202,11 +203,11 @@ cudaError_t launch_trace_bank(cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr
   if (gj && G > 1) {
     err = cudaMemsetAsync(gj, 0, sizeof(GridJob), st);
     if (err != cudaSuccess) return err;
-    void* args[] = {&g, &tr, &b, &e, &ov, &op, &ks, &save, &internal, &gj, &grid_min, &prof};
+    void* args[] = {&g, &tr, &b, &e, &ov, &op, &ks, &save, &internal, &gj, &grid_min, &prof, &bj};
     err = cudaLaunchCooperativeKernel((const void*)fn, dim3(G), dim3(32 * kTraceNW), args, smem, st);
   } else {
     fn<<<1, 32 * kTraceNW, smem, st>>>(g, tr, b, e, ov, op, ks, save, internal, gj, grid_min,
-                                       prof);
+                                       prof, nullptr);
     err = cudaGetLastError();
   }
   g_launches++;
@@ -557,6 +558,7 @@ struct pbh_heap {
   TraceImage* d_save = nullptr; // its level-0 image between launches
   u32 grid_min = kGridMin;
   unsigned long long* d_prof = nullptr;  // PBH_PROF: leader cycle breakdown
+  BatchJob* d_batch = nullptr;           // large-batch grid job (d >= kBigBatch)
   // staging for host traces
   u64 st_ops = 0, st_el = 0, st_out = 0;
   u8* d_kinds = nullptr;
@@ -630,7 +632,7 @@ pbh_status exec_trace(pbh_heap* h, u64 n_ops, pbh_trace_dev tr, u32* d_ov, u64* 
     CK(cudaEventRecord(h->ev0, h->stream));
     if (h->bank) {
       CK(launch_trace_bank(h->stream, h->H.dev, tr, begin, n_ops, d_ov, d_op, h->d_ks, h->d_save,
-                           internal, h->d_job, h->grid_min, h->d_prof));
+                           internal, h->d_job, h->grid_min, h->d_prof, h->d_batch));
     } else {
       CK(launch_trace_nt(h->nt, h->layout, h->stream, h->H.dev, tr, begin, n_ops, d_ov, d_op,
                          h->d_ks, internal, h->d_job));
@@ -767,7 +769,8 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
   // NEED_GROW is a kernel exit + relaunch)
   u32 nlev = 2;
   if (h->bank) {
-    h->H.base1 = 4ull * kBankQ;  // level 1 holds four push-buffer flushes
+    // level 1 holds four push-buffer flushes, or four whole large batches
+    h->H.base1 = std::max<u64>(4ull * kBankQ, 4 * std::min<u64>(d, 1ull << 26));
     while (nlev < 12 && (h->H.base1 << (2 * (nlev - 2))) < 2 * key_universe + 4 * kBankQ) ++nlev;
   }
   pbh_status st = init_heap(h->H, d, cap0, bc, h->nt, key_universe, debug_checks, nlev, nullptr);
@@ -791,6 +794,26 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
     if (e != cudaSuccess) return fail(set_err(PBH_CUDA, "level-0 image init failed"));
   }
   if (const char* e = getenv("PBH_GRID_MIN")) h->grid_min = std::max(2, atoi(e));
+  if (h->bank && h->d_job && d >= kBigBatch) {
+    // large batches: job block + staging / sort ping-pong / leader list
+    const u64 cap = std::min<u64>(d, 1ull << 26);
+    BatchJob hb{};
+    void* mem[6] = {};
+    const size_t sz[6] = {sizeof(BatchJob), cap * 4, cap * 8, cap * 4, cap * 8, cap * 4};
+    for (int i = 0; i < 6; ++i)
+      if (cudaMalloc(&mem[i], sz[i]) != cudaSuccess) return fail(set_err(PBH_OOM, "batch buffers"));
+    for (int i = 0; i < 6; ++i) h->H.allocs.push_back(mem[i]);
+    h->d_batch = (BatchJob*)mem[0];
+    hb.sk[0] = (u32*)mem[1];
+    hb.sp[0] = (u64*)mem[2];
+    hb.sk[1] = (u32*)mem[3];
+    hb.sp[1] = (u64*)mem[4];
+    hb.ll = (u32*)mem[5];
+    hb.stg_k = hb.sk[0];
+    hb.stg_p = hb.sp[0];
+    if (cudaMemcpy(h->d_batch, &hb, sizeof hb, cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(set_err(PBH_CUDA, "batch job init"));
+  }
   if (getenv("PBH_PROF") && cudaMalloc(&h->d_prof, 16 * sizeof(unsigned long long)) == cudaSuccess)
     cudaMemset(h->d_prof, 0, 16 * sizeof(unsigned long long));
   cudaEventCreate(&h->ev0);
@@ -811,9 +834,9 @@ pbh_status pbh_heap_destroy(pbh_heap* h) {
   if (h->d_prof) {
     unsigned long long pc[16];
     cudaMemcpy(pc, h->d_prof, sizeof pc, cudaMemcpyDeviceToHost);
-    fprintf(stderr, "pbh_prof cycles: validate %llu apply %llu bulk_cold %llu extract %llu refill %llu tail %llu pre %llu"
+    fprintf(stderr, "pbh_prof cycles: validate %llu apply %llu bulk_cold %llu extract %llu refill %llu tail %llu pre %llu big_sort %llu"
             " | sort %llu push_down %llu resolve1 %llu r2 %llu r3 %llu r4 %llu r5 %llu r6+ %llu\n",
-            pc[0], pc[1], pc[2], pc[3], pc[4], pc[5], pc[6], pc[8], pc[9], pc[10], pc[11], pc[12],
+            pc[0], pc[1], pc[2], pc[3], pc[4], pc[5], pc[6], pc[7], pc[8], pc[9], pc[10], pc[11], pc[12],
             pc[13], pc[14], pc[15]);
     cudaFree(h->d_prof);
   }

@@ -25,11 +25,141 @@ constexpr u32 kGridTile = 2048;   // outputs per streamed tile
 constexpr u32 kGridMin = 2048;    // smallest merge worth a grid job (measured sweep 2K..16K: 2K best)
 constexpr u32 kStreamMin = 64;    // smallest merge streamed through the windows by one CTA
 
+// Sort n entries (K, P) in shared memory by (p, k) with the whole CTA (K, P,
+// TK, TP hold the width n rounded up to a power of two >= 128): the warps
+// sort runs of 128 in registers (4 per lane, element r*32 + lane; bitonic
+// network, shuffles below stride 32), then merge-path rounds (one search and
+// M/NT outputs per thread) double the run width, ping-ponging through
+// (TK, TP). Slots n.. of the padded width are (~0, ~0): they sort last.
+template <int NW>
+DEV void cta_sort(u32* K, u64* P, u32 n, u32* TK, u64* TP) {
+  constexpr u32 NT = 32 * NW;
+  const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  u32 M = 128;
+  while (M < n) M <<= 1;
+  for (u32 run = w; run * 128 < M; run += NW) {
+    u64 p[4];
+    u32 k[4];
+#pragma unroll
+    for (u32 r = 0; r < 4; ++r) {
+      const u32 i = run * 128 + r * 32 + lane;
+      p[r] = i < n ? P[i] : ~0ull;
+      k[r] = i < n ? K[i] : 0xffffffffu;
+    }
+#pragma unroll
+    for (u32 size = 2; size <= 128; size <<= 1) {
+#pragma unroll
+      for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
+        if (stride >= 32) {
+          const u32 rs = stride / 32;
+#pragma unroll
+          for (u32 r = 0; r < 4; ++r) {
+            if (r & rs) continue;
+            const u32 i = r * 32 + lane;  // lower element of the pair
+            const bool up = (i & size) == 0;
+            const bool gt = less_pk(p[r | rs], k[r | rs], p[r], k[r]);
+            if (gt == up) {
+              const u64 tp = p[r];
+              p[r] = p[r | rs];
+              p[r | rs] = tp;
+              const u32 tk = k[r];
+              k[r] = k[r | rs];
+              k[r | rs] = tk;
+            }
+          }
+        } else {
+#pragma unroll
+          for (u32 r = 0; r < 4; ++r) {
+            const u32 i = r * 32 + lane;
+            const u32 ohi = __shfl_xor_sync(0xffffffffu, (u32)(p[r] >> 32), stride);
+            const u32 olo = __shfl_xor_sync(0xffffffffu, (u32)p[r], stride);
+            const u32 ok = __shfl_xor_sync(0xffffffffu, k[r], stride);
+            const u64 op = ((u64)ohi << 32) | olo;
+            const bool up = (i & size) == 0;
+            const bool lower = (lane & stride) == 0;
+            const bool other_less = less_pk(op, ok, p[r], k[r]);
+            if (lower == up ? other_less : !other_less) {
+              p[r] = op;
+              k[r] = ok;
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (u32 r = 0; r < 4; ++r) {
+      K[run * 128 + r * 32 + lane] = k[r];
+      P[run * 128 + r * 32 + lane] = p[r];
+    }
+  }
+  __syncthreads();
+  u32* sk = K;
+  u64* sp = P;
+  u32* dk = TK;
+  u64* dp = TP;
+  for (u32 wr = 128; wr < M; wr <<= 1) {
+    // each thread merges one contiguous range of M / NT outputs (one
+    // merge-path search per round)
+    const u32 per = M / NT;  // M >= 128 and NT <= 256: per >= 1 when M >= NT
+    for (u32 o0 = tid * per; o0 < M; o0 += per * NT) {
+      const u32 base = (o0 / (2 * wr)) * 2 * wr;
+      const u32 d = o0 - base;
+      const u32* ak = sk + base;
+      const u64* ap = sp + base;
+      const u32* bk = sk + base + wr;
+      const u64* bp = sp + base + wr;
+      u32 lo = d > wr ? d - wr : 0, hi = d < wr ? d : wr;
+      while (lo < hi) {
+        const u32 m = (lo + hi) >> 1;
+        if (less_pk(ap[m], ak[m], bp[d - 1 - m], bk[d - 1 - m]))
+          lo = m + 1;
+        else
+          hi = m;
+      }
+      u32 x = lo, y = d - lo;
+      u64 xa = x < wr ? ap[x] : ~0ull, yb = y < wr ? bp[y] : ~0ull;
+      u32 xk = x < wr ? ak[x] : 0xffffffffu, yk = y < wr ? bk[y] : 0xffffffffu;
+      for (u32 v = 0; v < per; ++v) {
+        const bool ta = x < wr && (y >= wr || less_pk(xa, xk, yb, yk));
+        if (ta) {
+          dk[o0 + v] = xk;
+          dp[o0 + v] = xa;
+          ++x;
+          xa = x < wr ? ap[x] : ~0ull;
+          xk = x < wr ? ak[x] : 0xffffffffu;
+        } else {
+          dk[o0 + v] = yk;
+          dp[o0 + v] = yb;
+          ++y;
+          yb = y < wr ? bp[y] : ~0ull;
+          yk = y < wr ? bk[y] : 0xffffffffu;
+        }
+      }
+    }
+    __syncthreads();
+    u32* t1 = sk;
+    sk = dk;
+    dk = t1;
+    u64* t2 = sp;
+    sp = dp;
+    dp = t2;
+  }
+  if (sk != K) {
+    for (u32 i = tid; i < n; i += NT) {
+      K[i] = sk[i];
+      P[i] = sp[i];
+    }
+    __syncthreads();
+  }
+}
+
 // Job word + descriptor in HBM (one per heap handle).
+struct BatchJob;
 struct GridJob {
   u32 seq;   // bumped by the leader to publish a job
   u32 done;  // helpers that finished the current job
-  u32 kind;  // 0 = merge, 1 = exit
+  u32 kind;  // 0 = merge, 1 = exit, 2 = validate batch, 3 = classify batch,
+             // 4 = sort chunks, 5 = merge pass (BatchJob in `ext`)
   u32 nblk;  // CTAs in the grid (leader included)
   const u32* ak;
   const u64* ap;
@@ -39,10 +169,37 @@ struct GridJob {
   u32 c;       // outputs: the first c of merge(A, B)
   u32 out_base;
   Sink sink;
+  BatchJob* ext;
+};
+
+// A large bulk_update batch handled by the whole grid (kinds 2-5). The leader
+// fills the fields and zeroes the counters before posting.
+constexpr u32 kSortChunk = 2048;  // elements per CTA-sorted chunk
+constexpr u32 kBigBatch = 8192;   // batches at least this large go to the grid
+struct BatchJob {
+  const u32* vals;
+  const u64* prios;
+  pbh_idx_entry* idx;
+  u64 universe;
+  u64 spl_p;
+  u32 spl_k, spl_inf;
+  u32 n, check, debug, c0;
+  // kind 3 outputs: entries for HBM (stg, (p, k) unsorted) and the batch
+  // positions the leader applies itself (level-0 slots or admitted)
+  u32* stg_k;
+  u64* stg_p;
+  u32* ll;
+  // kinds 4/5: sort src -> dst (run width `width` for kind 5)
+  u32* sk[2];
+  u64* sp[2];
+  u32 sort_n, width, src;
+  // counters (atomics)
+  u32 stg_n, ll_n, fresh, errs;
 };
 
 template <int NT>
 struct GridSmem {
+  GridJob sub;  // one piece of a merge pass
   u32 ak[kGridTile], bk[kGridTile], ok[kGridTile];
   u64 ap[kGridTile], bp[kGridTile], op[kGridTile];
   GridJob job;  // the current job, copied in by thread 0
@@ -121,10 +278,154 @@ DEV void grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u
   }
 }
 
+// Warp-aggregated append to a global counter: returns this lane's slot.
+DEV u32 warp_append(u32* ctr, bool want) {
+  const u32 m = __ballot_sync(0xffffffffu, want);
+  if (!m) return 0;
+  const u32 lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  u32 base = 0;
+  if (lane == leader) base = atomicAdd(ctr, (u32)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return base + __popc(m & ((1u << lane) - 1));
+}
+
+// kind 2: validate this CTA's slice of the batch (bucket_heap.cpp:127-136
+// preconditions): bit 0 unsorted, 1 key range, 2 dead value, 3 increase.
+template <int NT>
+DEV void batch_validate(BatchJob* X, u32 b, u32 G) {
+  const u32 n = X->n;
+  const u32 r0 = (u32)((u64)n * b / G), r1 = (u32)((u64)n * (b + 1) / G);
+  u32 bad = 0;
+  for (u32 j = r0 + threadIdx.x; j < r1; j += NT) {
+    const u32 k = X->vals[j];
+    if (X->check && j > 0 && X->vals[j - 1] >= k) bad |= 1;
+    if (k >= X->universe) {
+      bad |= 2;
+      continue;
+    }
+    const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(X->idx + k));
+    if (PBH_ST((u32)e.y) == PBH_ST_DEAD) bad |= 4;
+    if (X->debug && PBH_ST((u32)e.y) == PBH_ST_LIVE && X->prios[j] > e.x) bad |= 8;
+  }
+  bad = __reduce_or_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0 && bad) atomicOr(&X->errs, bad);
+}
+
+// kind 3: classify this CTA's slice. An improving element whose valid copy
+// is in a level-0 slot, or that splitter_0 admits, is listed for the leader
+// (it needs the shared-memory banks); any other goes straight to HBM: its
+// index entry becomes {p, LIVE, deep} and (k, p) is appended to the staging
+// run that will be sorted and pushed into S_1.
+template <int NT>
+DEV void batch_classify(BatchJob* X, u32 b, u32 G) {
+  const u32 n = X->n;
+  const u32 r0 = (u32)((u64)n * b / G), r1 = (u32)((u64)n * (b + 1) / G);
+  u32 fresh = 0;
+  for (u32 j0 = r0; j0 < r1; j0 += NT) {
+    const u32 j = j0 + threadIdx.x;
+    bool to_leader = false, to_hbm = false;
+    u32 k = 0;
+    u64 p = 0;
+    if (j < r1) {
+      k = X->vals[j];
+      p = X->prios[j];
+      const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(X->idx + k));
+      const u32 st = (u32)e.y;
+      const bool fr = PBH_ST(st) != PBH_ST_LIVE;
+      if (fr || p < e.x) {
+        const bool adm = X->spl_inf || p < X->spl_p || (p == X->spl_p && k <= X->spl_k);
+        if ((!fr && (st >> 2) < X->c0) || adm) {
+          to_leader = true;
+        } else {
+          to_hbm = true;
+          fresh += fr;
+          pbh_idx_entry ne;
+          ne.prio = p;
+          ne.state = PBH_ST_LIVE | (PBH_LOC_DEEP << 2);
+          ne.parent = 0;
+          reinterpret_cast<ulonglong2*>(X->idx)[k] = *reinterpret_cast<const ulonglong2*>(&ne);
+        }
+      }
+    }
+    const u32 ls = warp_append(&X->ll_n, to_leader);
+    if (to_leader) X->ll[ls] = j;
+    const u32 hs = warp_append(&X->stg_n, to_hbm);
+    if (to_hbm) {
+      X->stg_k[hs] = k;
+      X->stg_p[hs] = p;
+    }
+  }
+  fresh = __reduce_add_sync(0xffffffffu, fresh);
+  if ((threadIdx.x & 31) == 0 && fresh) atomicAdd(&X->fresh, fresh);
+}
+
+// kind 4: sort chunks of kSortChunk of sk/sp[src] in place (CTA-wide sort in
+// the GridSmem windows).
+template <int NT>
+DEV void batch_sort_chunks(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
+  const u32 n = X->sort_n;
+  u32* K = X->sk[X->src];
+  u64* P = X->sp[X->src];
+  for (u32 c0 = b * kSortChunk; c0 < n; c0 += G * kSortChunk) {
+    const u32 m = min(kSortChunk, n - c0);
+    for (u32 i = threadIdx.x; i < m; i += NT) {
+      cp_async4(&g.ak[i], K + c0 + i, true);
+      cp_async8(&g.ap[i], P + c0 + i);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    Blk<NT>::sync();
+    cta_sort<NT / 32>(g.ak, g.ap, m, g.bk, g.bp);
+    for (u32 i = threadIdx.x; i < m; i += NT) {
+      K[c0 + i] = g.ak[i];
+      P[c0 + i] = g.ap[i];
+    }
+    Blk<NT>::sync();
+  }
+}
+
+// kind 5: one merge pass over runs of `width` (src -> dst): this CTA's output
+// range, cut at pair boundaries, each piece one merge-path stream.
+template <int NT>
+DEV void batch_merge_pass(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g, u32* scratch) {
+  const u32 n = X->sort_n, w = X->width;
+  const u32 r0 = (u32)((u64)n * b / G), r1 = (u32)((u64)n * (b + 1) / G);
+  const u32 s = X->src;
+  u32 lo = r0;
+  while (lo < r1) {
+    const u32 base = lo / (2 * w) * (2 * w);
+    const u32 hi = min(r1, base + 2 * w);
+    const u32 na = min(w, n - base), nb = base + w < n ? min(w, n - base - w) : 0;
+    const Run A{X->sk[s] + base, X->sp[s] + base, na};
+    const Run B{X->sk[s] + base + na, X->sp[s] + base + na, nb};
+    const u32 d0 = lo - base, d1 = hi - base;
+    const u32 a0 = d0 == 0 ? 0 : merge_split<NT>(A, B, d0, scratch);
+    const u32 a1 = merge_split<NT>(A, B, d1, scratch);
+    if (threadIdx.x == 0) {
+      g.sub.ak = A.k;
+      g.sub.ap = A.p;
+      g.sub.bk = B.k;
+      g.sub.bp = B.p;
+      g.sub.sink = Sink{X->sk[s ^ 1] + base, X->sp[s ^ 1] + base, 0xffffffffu, nullptr, nullptr};
+    }
+    Blk<NT>::sync();
+    grid_stream<NT>(g.sub, a0, a1, d0 - a0, d1 - a1, d0, g);
+    Blk<NT>::sync();
+    lo = hi;
+  }
+}
+
 // This CTA's share (block b of G) of the current job.
 template <int NT>
 DEV void grid_share(const GridJob& J, u32 b, GridSmem<NT>& g, u32* scratch) {
   const u32 G = J.nblk;
+  switch (J.kind) {
+    case 2: return batch_validate<NT>(J.ext, b, G);
+    case 3: return batch_classify<NT>(J.ext, b, G);
+    case 4: return batch_sort_chunks<NT>(J.ext, b, G, g);
+    case 5: return batch_merge_pass<NT>(J.ext, b, G, g, scratch);
+    default: break;
+  }
   const u32 r0 = (u32)((u64)J.c * b / G), r1 = (u32)((u64)J.c * (b + 1) / G);
   if (r0 >= r1) return;
   const Run A{J.ak, J.ap, J.na}, B{J.bk, J.bp, J.nb};
@@ -192,6 +493,7 @@ NOINL void grid_run(GridJob* gj, u32 G, u32 kind, const Run& A, const Run& B, u3
     J.c = c;
     J.out_base = out_base;
     J.sink = sink;
+    J.ext = g.job.ext;
     // descriptor fields first, then the sequence word (release)
     gj->kind = J.kind;
     gj->nblk = J.nblk;
@@ -204,6 +506,7 @@ NOINL void grid_run(GridJob* gj, u32 G, u32 kind, const Run& A, const Run& B, u3
     gj->c = J.c;
     gj->out_base = J.out_base;
     gj->sink = J.sink;
+    gj->ext = J.ext;
     gj->done = 0;
     const u32 s = g.seq + 1;  // the host zeroes the job word before each launch
     g.seq = s;

@@ -104,8 +104,9 @@ class Engine:
         if isinstance(batch, tuple) and len(batch) == 2 and hasattr(batch[0], "__len__"):
             vals, prios = batch
         else:
-            vals = [e[0] for e in batch]
-            prios = [e[1] for e in batch]
+            pairs = [tuple(e) for e in batch]  # Element or (value, priority)
+            vals = [e[0] for e in pairs]
+            prios = [e[1] for e in pairs]
         v = np.ascontiguousarray(vals, dtype=np.uint32)
         p = np.ascontiguousarray(prios, dtype=np.uint64)
         raise_for(_lib.lib().pbh_heap_bulk_update(self._h, _ptr(v, U32P), _ptr(p, U64P), len(v)))
