@@ -10,6 +10,10 @@ persistent CTA of 4 warps (k_sssp_bank). value = edges relaxed by all ranks / ma
 device time. The single-source (configs[2]) latency-bound number is reported
 in "single_source".
 
+The line also carries "bulk_update": BASELINE C4 at d = 65536 into a
+2^26-key heap (the other half of the metric), with its own roofline and the
+reference's Engine::bulk_update timed on a sample ("cpu_baseline").
+
 --impl reference times the reference's own CPU par_dijkstra
 (oracle/_ref = /root/reference/proj/src compiled unmodified) on all host
 threads for the same workload (bounded sample per step), rank 0 only.
@@ -44,6 +48,7 @@ def parse():
     ap.add_argument("--deg", type=int, default=DEG_DEFAULT)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-bulk", action="store_true", help="skip the C4 bulk_update leg")
     ap.add_argument("--cpu-sample-sources", type=int, default=0,
                     help="sources in the CPU baseline sample (0 = one per host thread)")
     return ap.parse_args()
@@ -208,6 +213,55 @@ def run_reference_arm(args, D):
     print(json.dumps(out), flush=True)
 
 
+# ------------------------------------------------------------- bulkUpdate leg
+def bulk_update_leg(dev, peak, cpu=True, log2n=26, d=65536, n_batches=64):
+    """BASELINE C4 at its largest batch: bulk_update batches of d distinct
+    live keys (strict decreases) into a 2^26-key heap. Device time of the
+    batches only (the prefill is not timed). Roofline: 24 B
+    per update (key + priority read once, written once)."""
+    import paper_1908_09378_b200 as P
+    from paper_1908_09378_b200 import gen
+
+    n = 1 << log2n
+    pr = gen.sweep_prefill(n, 4)
+
+    class T:
+        pass
+    t = T()
+    t.kinds = np.full(n // d, ord("B"), np.uint8)
+    t.offsets = np.arange(n // d + 1, dtype=np.uint64) * d
+    t.vals = np.arange(n, dtype=np.uint32)
+    t.prios = pr.copy()
+    eng = P.Engine(P.EngineConfig(d=d, debug_assertions=False, key_universe=n, device=dev))
+    eng.run_trace(t)  # prefill
+    v, p = gen.sweep_batches(n, d, n_batches, 5, pr)
+    t.kinds = np.full(n_batches, ord("B"), np.uint8)
+    t.offsets = np.arange(n_batches + 1, dtype=np.uint64) * d
+    t.vals, t.prios = v, p
+    ms = eng.run_trace(t).metrics.wall_ms
+    eng.close()
+    ups = len(v) / (ms / 1e3)
+    out = {"metric": "bulk_update_updates_per_sec", "value": ups, "unit": "updates/s",
+           "config": {"workload": "BASELINE C4: bulk_update sweep into a 2^26-key heap",
+                      "heap_keys": n, "d": d, "batches": n_batches, "updates": len(v)},
+           "ms": ms,
+           "roofline": {"bound": "hbm", "achieved": 24 * ups / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": 24 * ups / 1e9 / peak, "alg_bytes_per_update": 24,
+                        "kernel": "k_trace_bank<4,8,4> + grid helpers (cooperative, 148 CTAs)"}}
+    if cpu:
+        from oracle import oracle as O
+        if O.ref_available():
+            # reference Engine::bulk_update on a 2^22-key sample, 16 batches
+            ns = 1 << 22
+            prs = gen.sweep_prefill(ns, 4)
+            vs, ps = gen.sweep_batches(ns, d, 16, 5, prs.copy())
+            secs = O.ref_bulk_sweep(d, np.arange(ns, dtype=np.uint32), prs, vs, ps)
+            out["cpu_baseline"] = {"value": len(vs) / secs, "unit": "updates/s", "cores": 1,
+                                   "kind": "reference",
+                                   "sample": f"reference Engine::bulk_update, 2^22-key prefill, 16 batches of d={d}, {secs:.1f} s"}
+    return out
+
+
 # ------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -303,6 +357,10 @@ def run_pbh(args, D):
                    "sample": f"reference par_dijkstra (oracle/_ref), {n_s} of the {S} sources, "
                              f"one per host thread, {s:.1f} s"}
 
+    bulk = None
+    if D.rank == 0 and not args.no_bulk:
+        bulk = bulk_update_leg(dev, peak, cpu=(D.world == 1 and not args.no_cpu_baseline))
+
     if D.rank == 0:
         out = {
             "metric": "sssp_edges_relaxed_per_sec", "value": value, "unit": "edges/s",
@@ -326,6 +384,7 @@ def run_pbh(args, D):
             "gpu_launches": int(launches),
             "clocks": clk,
             "single_source": single,
+            "bulk_update": bulk,
             "parity": {"spine_dist": bool(ok_spine), "parent_tree": tree is None,
                        "reached": reached, "e2e_spine": bool(e2e_ok)},
             "gen_s": gen_s,
