@@ -15,7 +15,6 @@
 #include <vector>
 
 #include "../../include/pbh_gpu.h"
-#include "pbh_fast.cuh"
 #include "pbh_bank.cuh"
 #include "pbh_bf.cuh"
 #include "pbh_multi.cuh"
@@ -43,7 +42,6 @@ pbh_status set_err(pbh_status s, const std::string& msg) {
   } while (0)
 
 constexpr int VT = 4;
-constexpr int kFastCap0 = 1024;  // B_0 capacity of the fast SSSP path (static smem)
 constexpr u32 kSmemLimit = 227 * 1024;
 
 u64 pow2_at_least(u64 x) {
@@ -237,39 +235,6 @@ cudaError_t launch_sssp_nt(int nt, const SmLayout& L, cudaStream_t st, u32 grid,
   }
 }
 
-FastLayout make_fast_layout(u32 cap0) {
-  FastLayout L{};
-  u32 off = 0;
-  L.off_hs = off; off += a16(sizeof(HeapSmem<32, VT>));
-  for (int s = 0; s < 2; ++s) { L.off_bk[s] = off; off += a16((u64)cap0 * 4); }
-  for (int s = 0; s < 2; ++s) { L.off_bp[s] = off; off += a16((u64)cap0 * 8); }
-  for (int s = 0; s < 2; ++s) { L.off_bt[s] = off; off += a16(cap0); }
-  L.off_sk = off; off += a16(kFastS0 * 4);
-  L.off_sp = off; off += a16(kFastS0 * 8);
-  L.off_sv = off; off += a16(kFastS0);
-  L.off_tk = off; off += a16(kFastS0 * 4);
-  L.off_tp = off; off += a16(kFastS0 * 8);
-  L.off_pk = off; off += a16((u64)2 * kFastS0 * 4);
-  L.off_pp = off; off += a16((u64)2 * kFastS0 * 8);
-  L.off_cpos = off; off += a16(((u64)std::max<u32>(cap0, kFastS0) + 64) * 4);
-  L.off_ck = off; off += a16(kChunk * 4);
-  L.off_cp = off; off += a16(kChunk * 8);
-  L.off_co = off; off += a16(kChunk * 8);
-  L.off_cs = off; off += a16(kChunk * 4);
-  L.off_kf = off; off += a16(kChunk);
-  L.total = off;
-  return L;
-}
-
-cudaError_t launch_sssp_fast(const FastLayout& L, cudaStream_t st, u32 grid, pbh_heap_dev* heaps,
-                             const u64* off, const u32* tgt, const u32* w, u32 V, const u32* src,
-                             u64* dist, u32* settled, SsspState* sst, u32 dag, u32 maxdeg, u32 d) {
-  auto fn = k_sssp_fast<kFastCap0, VT>;
-  static const u32 xp = getenv("PBH_XP") ? (u32)atoi(getenv("PBH_XP")) : 0u;
-  fn<<<grid, 32, 0, st>>>(heaps, off, tgt, w, V, src, dist, settled, sst, dag, maxdeg, d, L, xp);
-  g_launches++;
-  return cudaGetLastError();
-}
 
 // Banked level-0 SSSP engine variants: NW warps per source, KI slots per
 // thread, level 0 = 32*NW*KI = 1024 slots.
@@ -1139,8 +1104,7 @@ struct pbh_sssp_ctx {
   u32 cap0 = 0;
   u64 max_sources = 0;
   SmLayout layout{};
-  FastLayout flayout{};
-  bool fast = true;   // warp engines (lane-banked or sorted-B_0); false = CTA engine
+  bool fast = true;   // banked engine (false: the sorted-B_0 CTA engine, PBH_SSSP_ENGINE=cta)
   bool lane = true;   // banked level 0 (default)
   int bank_nw = 1;    // warps per source of the banked engine
   void* d_save = nullptr;
@@ -1224,20 +1188,13 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
   c->d = std::min<u64>(c->d, std::max<u64>(1, md ? md : 1));  // batches never exceed a row
   c->nt = pick_nt(std::max<u64>(c->d, std::min<u64>(md, 1024)));
   c->cap0 = pick_cap0(c->d);
-  if (const char* e = getenv("PBH_SSSP_ENGINE")) {
-    c->fast = std::string(e) != "cta";
-    c->lane = std::string(e) == "lane";
-  }
+  if (const char* e = getenv("PBH_SSSP_ENGINE")) c->fast = c->lane = std::string(e) != "cta";
   if (c->lane) {
     c->bank_nw = 4;
     if (const char* e = getenv("PBH_SSSP_NW")) c->bank_nw = atoi(e);
     if (c->bank_nw != 1 && c->bank_nw != 2 && c->bank_nw != 4 && c->bank_nw != 8) c->bank_nw = 4;
     c->cap0 = kBankC0 / 2;
     c->nt = 32 * c->bank_nw;
-  } else if (c->fast) {
-    c->cap0 = kFastCap0;
-    c->nt = 32;
-    c->flayout = make_fast_layout(c->cap0);
   }
   const u32 bc = (u32)pow2_at_least(std::max<u64>(c->d, 2));
   c->layout = make_layout(c->nt, c->cap0, bc, (u32)c->d, true);
@@ -1328,10 +1285,6 @@ pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n
                              c->d_tgt, c->d_w, c->V, c->d_src, c->d_dist, c->d_settled, c->d_sst,
                              c->d_save, dag_mode ? 1 : 0, c->max_deg,
                              (u32)std::min<u64>(c->d, 0xffffffffu)));
-    } else if (c->fast) {
-      CK(launch_sssp_fast(c->flayout, c->stream, (u32)n_sources, c->d_heaps, c->d_off, c->d_tgt,
-                          c->d_w, c->V, c->d_src, c->d_dist, c->d_settled, c->d_sst,
-                          dag_mode ? 1 : 0, c->max_deg, (u32)std::min<u64>(c->d, 0xffffffffu)));
     } else {
       CK(launch_sssp_nt(c->nt, c->layout, c->stream, (u32)n_sources, c->d_heaps, c->d_off,
                         c->d_tgt, c->d_w, c->V, c->d_src, c->d_dist, c->d_settled, c->d_sst,
@@ -1379,13 +1332,9 @@ pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n
     SsspState s0;
     cudaMemcpy(&s0, c->d_sst, sizeof s0, cudaMemcpyDeviceToHost);
     const double r = s0.rounds ? (double)s0.rounds : 1.0;
-    if (c->lane)
-      fprintf(stderr, "phases cyc/round (lane): extract %.0f relax %.0f apply %.0f cold %.0f tail %.0f\n",
-              s0.phase[0] / r, s0.phase[1] / r, s0.phase[2] / r, s0.phase[3] / r, s0.phase[4] / r);
-    else
-    fprintf(stderr, "phases cyc/round: extract %.0f relax %.0f kill %.0f append %.0f tail %.0f | flush %.0f (n=%llu) smin %.0f | pf_hits %.3f\n",
-            s0.phase[0] / r, s0.phase[1] / r, s0.phase[2] / r, s0.phase[3] / r, s0.phase[4] / r,
-            s0.phase[5] / r, (unsigned long long)s0.pad2, s0.phase[6] / r, s0.phase[7] / r);
+    if (!c->lane)
+      fprintf(stderr, "phases cyc/round (cta): %.0f %.0f %.0f %.0f %.0f\n", s0.phase[0] / r,
+              s0.phase[1] / r, s0.phase[2] / r, s0.phase[3] / r, s0.phase[4] / r);
   }
   return PBH_OK;
 }
