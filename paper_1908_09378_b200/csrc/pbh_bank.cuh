@@ -414,7 +414,10 @@ struct BankHeap {
       n += tot;
     }
     Bk::sync();
-    bitonic_sort<B>(SK, SP, n);
+    {
+      auto& SS = bank_smem<NW, KI, VT, MW>();  // LDS-addressed sort (see flush_q)
+      cta_sort<NW>(&SS.bk[0][0], &SS.bp[0][0], n, SS.sk, SS.sp);
+    }
     const u32 keep = n < (u32)C0 / 2 ? n : (u32)C0 / 2;
     if (n > keep) {
       if (tid == 0) {
