@@ -61,11 +61,25 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.backend = None
+        self.device = self.local
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            n_dev = torch.cuda.device_count()
+            if n_dev >= self.world:
+                # one process per GPU; NCCL carries only the barrier and the
+                # max-over-ranks of the timings (no collective on the data path)
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+                self.backend = "nccl"
+            else:
+                # more ranks than GPUs (a functional check on a small box):
+                # ranks share devices, timings reduce over gloo
+                self.device = self.local % max(n_dev, 1)
+                torch.cuda.set_device(self.device)
+                dist.init_process_group("gloo")
+                self.backend = "gloo"
             self.pg = dist
 
     def barrier(self):
@@ -76,7 +90,7 @@ class Dist:
         if not self.pg:
             return x
         import torch
-        t = torch.tensor([float(x)], device="cuda")
+        t = torch.tensor([float(x)], device="cuda" if self.backend == "nccl" else "cpu")
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
 
@@ -279,7 +293,7 @@ def run_pbh(args, D):
     import paper_1908_09378_b200 as P
     from paper_1908_09378_b200 import _lib, gen
 
-    dev = D.local
+    dev = D.device
     t0 = time.time()
     g = gen.band(args.v, args.deg, 2)
     gen_s = time.time() - t0
