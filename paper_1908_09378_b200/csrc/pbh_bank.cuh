@@ -95,6 +95,10 @@ DEV BankSmem<NW, KI, VT, MW>& bank_smem() {
   return *reinterpret_cast<BankSmem<NW, KI, VT, MW>*>(dyn);
 }
 
+// ceil(a / b) out of line: the integer division stays off the hot path
+// (ptxas otherwise if-converts it into every round)
+__device__ __noinline__ u32 ceil_div_cold(u32 a, u32 b) { return (a + b - 1) / b; }
+
 // warp argmin of (p, k) over lanes with `has`; returns the winning lane.
 DEV u32 warp_argmin(bool& has, u64& p, u32& k) {
   const u32 hi = has ? (u32)(p >> 32) : 0xffffffffu;
@@ -821,7 +825,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
     SPROF(6);
     if (cold_fail || fail_bad || fail_ovf) break;
     // bulk_update batches of <= d (sssp.cpp:59-64)
-    if (n_imp) ops += n_imp <= d ? 1u : (n_imp + d - 1) / d;
+    if (n_imp) ops += n_imp <= d ? 1u : ceil_div_cold(n_imp, d);
   }
   cp_async_wait_all();
 #undef SPROF

@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
       }
     }
     if (cold_fail || fail_bad || fail_ovf) break;
-    if (n_imp) ops += n_imp <= d ? 1u : (n_imp + d - 1) / d;
+    if (n_imp) ops += n_imp <= d ? 1u : ceil_div_cold(n_imp, d);
   }
   H.occm = occm;
   H.live = live;
