@@ -1041,9 +1041,15 @@ __global__ void __launch_bounds__(32 * NW, 1)
       // pass 1: validate (no mutation)
       bool bad_sort = false, bad_key = false, bad_dead = false, bad_inc = false;
       // 4 elements per thread per step: their loads are all in flight at once
+      // the first pass's element, index entry and priority are kept for
+      // pass 2 (no mutation in between)
+      u32 v_first = 0;
+      u64 p_first = 0;
+      ulonglong2 e_first = make_ulonglong2(0, 0);
       for (u32 j0 = tid; !big && j0 < n; j0 += 4 * B) {
         u32 kk[4], kp[4];
         ulonglong2 e[4];
+        if (j0 == tid) p_first = prios[tid];
 #pragma unroll
         for (u32 t = 0; t < 4; ++t) {
           const u32 j = j0 + t * B;
@@ -1069,6 +1075,10 @@ __global__ void __launch_bounds__(32 * NW, 1)
           if (PBH_ST((u32)e[t].y) == PBH_ST_DEAD) bad_dead = true;
           if (debug && PBH_ST((u32)e[t].y) == PBH_ST_LIVE && prios[j] > e[t].x) bad_inc = true;
         }
+        if (j0 == tid) {
+          v_first = kk[0];
+          e_first = e[0];
+        }
       }
       if (!big) TPROF(6);
       const u32 bad = (u32)__syncthreads_or(bad_sort) | ((u32)__syncthreads_or(bad_key) << 1) |
@@ -1085,10 +1095,16 @@ __global__ void __launch_bounds__(32 * NW, 1)
       u64 nx_c = 0;
       ulonglong2 nx_e = make_ulonglong2(0, 0);
       if (tid < m_apply) {
-        const u32 jj = lst ? lst[tid] : tid;
-        nx_u = vals[jj];
-        nx_c = prios[jj];
-        nx_e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + nx_u));
+        if (big) {
+          const u32 jj = lst[tid];
+          nx_u = vals[jj];
+          nx_c = prios[jj];
+          nx_e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + nx_u));
+        } else {
+          nx_u = v_first;
+          nx_c = p_first;
+          nx_e = e_first;
+        }
       }
       for (u32 base = 0; base < m_apply; base += B) {
         const bool cold_now = evict_due || qn > (u32)(kBankQ - B);
