@@ -1332,6 +1332,11 @@ pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n
     SsspState s0;
     cudaMemcpy(&s0, c->d_sst, sizeof s0, cudaMemcpyDeviceToHost);
     const double r = s0.rounds ? (double)s0.rounds : 1.0;
+    if (c->multi)
+      fprintf(stderr, "multi phases cyc/batch: thresholds %.0f select %.0f prefix+commit %.0f "
+              "pass-top(cold) %.0f gathers+binsearch %.0f atomics+apply+exchange %.0f tail %.0f loop %.0f\n",
+              s0.phase[0] / r, s0.phase[1] / r, s0.phase[2] / r, s0.phase[3] / r, s0.phase[4] / r,
+              s0.phase[5] / r, s0.phase[6] / r, s0.phase[7] / r);
     if (!c->lane)
       fprintf(stderr, "phases cyc/round (cta): %.0f %.0f %.0f %.0f %.0f\n", s0.phase[0] / r,
               s0.phase[1] / r, s0.phase[2] / r, s0.phase[3] / r, s0.phase[4] / r);

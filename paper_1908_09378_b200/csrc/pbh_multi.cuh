@@ -178,11 +178,24 @@ __global__ void __launch_bounds__(32 * NW, 1)
   bool evict_due = Bk::any(__popc(occm) > (int)(KI - PE), hc.scr());
   bool fail_bad = false, fail_ovf = false, cold_fail = false;
   u32 pass_id = 0;
+  u64 mph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long mpt = clock64();
+#ifdef PBH_PROF_BUILD
+#define MPROF(i)                     \
+  {                                  \
+    const long long t1_ = clock64(); \
+    mph[i] += (u64)(t1_ - mpt);      \
+    mpt = t1_;                       \
+  }
+#else
+#define MPROF(i)
+#endif
   while (live > 0) {
     if (!grow_ok || (u64)qn + deep_n > grow_at) {
       need_grow = true;
       break;
     }
+    MPROF(7);
     // ---- the thresholds: L (level-0 minimum) and T (min of p + minout)
     if (rescan_due) multi_rescan<B, KI>(L, tid, occm, lhas, lmin_p, lmin_k, lmin_s, tmin);
     rescan_due = false;
@@ -205,6 +218,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
     u64 T = x.t;
     if (!L.spl_inf) T = min(T, L.spl_p + 1);
     const u64 Lp = x.p;
+    MPROF(0);
     // ---- select this bank's settled slots (OUT or IN criterion)
     u32 sel = 0;
     {
@@ -235,6 +249,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
       }
     }
     Bk::sync();
+    MPROF(1);
     // ---- edge offsets of the batch rows
     u32 te;
     {
@@ -272,6 +287,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
     ++rounds;
     ops += nb;
     live -= nb;
+    MPROF(2);
     // ---- relax the flattened rows in passes of 256 edges
     u32 n_imp = 0;
     for (u32 base = 0; base < te; base += kBankPass) {
@@ -287,6 +303,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
           break;
         }
       }
+      MPROF(3);
       u32 uu[PE], ww[PE], vv[PE];
       u64 pv[PE];
       bool in[PE];
@@ -331,6 +348,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
       asm volatile("" ::: "memory");
       if (rescan_due) multi_rescan<B, KI>(L, tid, occm, lhas, lmin_p, lmin_k, lmin_s, tmin);
       rescan_due = false;
+      MPROF(4);
       // phase A: candidates lower the index priority (64-bit atomicMin)
       bool imp[PE];
       u64 cand[PE];
@@ -400,6 +418,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
         }
         idx[u].state = nst;
       }
+      MPROF(5);
       ++pass_id;
       const u32 ev = (u32)__popc(occm) > (u32)KI - PE ? 1u : 0u;
       const BankOffer r = bank_exchange<NW, KI, VT, true>(
@@ -420,6 +439,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
         break;
       }
     }
+    MPROF(6);
     if (cold_fail || fail_bad || fail_ovf) break;
     if (n_imp) ops += n_imp <= d ? 1u : ceil_div_cold(n_imp, d);
   }
@@ -444,7 +464,10 @@ __global__ void __launch_bounds__(32 * NW, 1)
   if (tid == 0) sm.ops = H.pushes;
   Bk::sync();
   hc.store();
+#undef MPROF
+  (void)mpt;
   if (tid == 0) {
+    for (int i = 0; i < 8; ++i) my->phase[i] += mph[i];
     my->n_settled = n_settled;
     my->rounds = rounds;
     my->started = 1;
