@@ -463,7 +463,7 @@ struct BankHeap {
 // par_dijkstra with one CTA (NW warps) per source and a banked level 0.
 // The hot loop keeps all state in locals (registers); the BankHeap object is
 // only the hand-off to the cold-path methods.
-template <int NW, int KI, int VT>
+template <int NW, int KI, int VT, int PASS = kBankPass>
 __global__ void __launch_bounds__(32 * NW, 1)
     k_sssp_bank(pbh_heap_dev* heaps, const u64* __restrict__ off, const u32* __restrict__ tgt,
                 const u32* __restrict__ wt, u32 V, const u32* sources, u64* dist, u32* settled,
@@ -474,7 +474,10 @@ __global__ void __launch_bounds__(32 * NW, 1)
   using Bk = Blk<BH::B>;
   constexpr u32 B = BH::B;
   constexpr u32 C0 = BH::C0;
-  constexpr u32 PE = BH::PE;
+  // edges per thread per pass: PASS = 256 for dense rows; the low-degree
+  // variant (grids) uses one warp and PASS = 32 (one edge per lane)
+  constexpr u32 PE = PASS / B;
+  static_assert(PE >= 1 && PE * B == PASS && KI >= (int)PE, "pass shape");
   BankSmem<NW, KI, VT>& S = bank_smem<NW, KI, VT>();
   SsspState* my = sst + blockIdx.x;
   if (my->status != 0 && my->status != 7) return;
@@ -635,14 +638,14 @@ __global__ void __launch_bounds__(32 * NW, 1)
     const u32 deg = cur.deg;
     const u32 te = (tid + rot) & (B - 1);  // this thread's edge offset within a group of B
     bool cold_fail = false;
-    for (u32 done = 0; done < deg; done += kBankPass) {
-      const bool last = done + kBankPass >= deg;
+    for (u32 done = 0; done < deg; done += PASS) {
+      const bool last = done + PASS >= deg;
       const u32 rem = deg - done;
       const u64 base = rb + done;
-      if (evict_due || qn > (u32)(kBankQ - kBankPass)) {
+      if (evict_due || qn > (u32)(kBankQ - PASS)) {
         BANK_TO_H();
         if (evict_due) H.evict();
-        if (!hc.failed() && H.qn > (u32)(kBankQ - kBankPass)) H.flush_q();
+        if (!hc.failed() && H.qn > (u32)(kBankQ - PASS)) H.flush_q();
         BANK_FROM_H();
         if (evict_due) rescan_due = false;
         evict_due = false;

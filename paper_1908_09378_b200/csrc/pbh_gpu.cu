@@ -255,16 +255,16 @@ size_t bank_save_bytes() {
   return sizeof(BankL0<32 * NW, BankCfg<NW>::KI>);
 }
 size_t bank_save_bytes_nw(int nw) {
-  return nw == 1 ? bank_save_bytes<1>() : nw == 2 ? bank_save_bytes<2>()
+  return nw <= 1 ? bank_save_bytes<1>() : nw == 2 ? bank_save_bytes<2>()
          : nw == 4 ? bank_save_bytes<4>() : bank_save_bytes<8>();
 }
 
-template <int NW>
+template <int NW, int PASS = kBankPass>
 cudaError_t launch_sssp_bank(cudaStream_t st, u32 grid, pbh_heap_dev* heaps, const u64* off,
                              const u32* tgt, const u32* w, u32 V, const u32* src, u64* dist,
                              u32* settled, SsspState* sst, void* save, u32 dag, u32 maxdeg, u32 d) {
   constexpr int KI = BankCfg<NW>::KI;
-  auto fn = k_sssp_bank<NW, KI, VT>;
+  auto fn = k_sssp_bank<NW, KI, VT, PASS>;
   const int smem = (int)sizeof(BankSmem<NW, KI, VT>);
   static bool attr = false;
   if (!attr) {
@@ -320,6 +320,8 @@ cudaError_t launch_sssp_bank_nw(int nw, cudaStream_t st, u32 grid, pbh_heap_dev*
                                 const u32* src, u64* dist, u32* settled, SsspState* sst,
                                 void* save, u32 dag, u32 maxdeg, u32 d) {
   switch (nw) {
+    case 0:  // one warp, 32-edge passes: low-degree graphs
+      return launch_sssp_bank<1, 32>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
     case 1: return launch_sssp_bank<1>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
     case 2: return launch_sssp_bank<2>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
     case 4: return launch_sssp_bank<4>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
@@ -1192,9 +1194,10 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
   if (c->lane) {
     c->bank_nw = 4;
     if (const char* e = getenv("PBH_SSSP_NW")) c->bank_nw = atoi(e);
-    if (c->bank_nw != 1 && c->bank_nw != 2 && c->bank_nw != 4 && c->bank_nw != 8) c->bank_nw = 4;
+    if (c->bank_nw != 0 && c->bank_nw != 1 && c->bank_nw != 2 && c->bank_nw != 4 && c->bank_nw != 8)
+      c->bank_nw = 4;
     c->cap0 = kBankC0 / 2;
-    c->nt = 32 * c->bank_nw;
+    c->nt = 32 * std::max(c->bank_nw, 1);
   }
   const u32 bc = (u32)pow2_at_least(std::max<u64>(c->d, 2));
   c->layout = make_layout(c->nt, c->cap0, bc, (u32)c->d, true);
