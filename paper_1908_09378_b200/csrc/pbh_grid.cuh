@@ -176,6 +176,10 @@ struct GridJob {
 // fills the fields and zeroes the counters before posting.
 constexpr u32 kSortChunk = 2048;  // elements per CTA-sorted chunk
 constexpr u32 kBigBatch = 8192;   // batches at least this large go to the grid
+#ifndef PBH_POLL_MAX_NS
+#define PBH_POLL_MAX_NS 64
+#endif
+constexpr u32 kPollMaxNs = PBH_POLL_MAX_NS;  // job-word polling backoff cap
 struct BatchJob {
   const u32* vals;
   const u64* prios;
@@ -444,10 +448,10 @@ DEV void grid_helper_loop(GridJob* gj, GridSmem<NT>& g, u32* scratch) {
   for (;;) {
     if (threadIdx.x == 0) {
       u32 s;
-      u32 backoff = 32;
+      u32 backoff = 16;
       while ((s = ld_acquire(&gj->seq)) == seen) {
         __nanosleep(backoff);
-        backoff = backoff < 256 ? backoff * 2 : 256;
+        backoff = backoff < kPollMaxNs ? backoff * 2 : kPollMaxNs;
       }
       g.seq = s;
       // the descriptor, read through L2 (never a stale L1 line)
@@ -518,10 +522,10 @@ NOINL void grid_run(GridJob* gj, u32 G, u32 kind, const Run& A, const Run& B, u3
   grid_share<NT>(g.job, 0, g, scratch);
   Bk::sync();
   if (threadIdx.x == 0) {
-    u32 backoff = 32;
+    u32 backoff = 16;
     while (ld_acquire(&gj->done) < G - 1) {
       __nanosleep(backoff);
-      backoff = backoff < 256 ? backoff * 2 : 256;
+      backoff = backoff < kPollMaxNs ? backoff * 2 : kPollMaxNs;
     }
     __threadfence();
   }
