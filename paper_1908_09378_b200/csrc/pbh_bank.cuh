@@ -87,6 +87,10 @@ struct BankSmem {
   BankOffer ex[2][NW];  // per-pass exchange (parity double-buffered)
   u8 dirty[2][B];       // decreased-bank flags (parity double-buffered)
   HeapSmem<B, VT> hs;
+#ifdef PBH_XPROF
+  long long xarr[2][NW];  // per-warp barrier arrival clocks (diagnostics)
+  long long xph[2][NW][8];  // per-warp phase cycles of this pass (PBH_PROF_BUILD)
+#endif
 };
 
 template <int NW, int KI, int VT, bool MW = false>
@@ -141,7 +145,8 @@ DEV void bank_rescan(const BankL0<B, KI, MW>& L, u32 tid, u32 occm, bool& lhas, 
 // and row, and the sums of the counters. One barrier. Counters are packed
 // 9 bits each (every one is <= 256 per pass): c0 = fresh | nimp << 9 |
 // ovf << 18, c1 = nq | evict << 9 | bad << 18 (the last two per-thread flags).
-__device__ unsigned long long g_xprof[8];  // PBH_PHASES: exchange breakdown (thread 0, block 0)
+__device__ unsigned long long g_xprof[16];
+__device__ unsigned long long g_xprof2[8];  // PBH_PHASES: exchange breakdown (thread 0, block 0)
 
 template <int NW, int KI, int VT, bool MW = false>
 DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u32 deg, u32 c0,
@@ -150,7 +155,12 @@ DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u
   const u32 tid = threadIdx.x;
   const u32 lane = tid & 31, w = tid >> 5;
 #ifdef PBH_XPROF
-  const long long xa = clock64();
+  auto clk = []() {
+    long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)::"memory");
+    return c;
+  };
+  const long long xa = clk();
 #endif
   bool h = has;
   u64 wp = p;
@@ -193,11 +203,12 @@ DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u
     return r;
   } else {
 #ifdef PBH_XPROF
-    const long long xb = clock64();
+    const long long xb = clk();
+    if (lane == 0) S.xarr[par][w] = xb;
 #endif
     __syncthreads();
 #ifdef PBH_XPROF
-    const long long xc = clock64();
+    const long long xc = clk();
 #endif
     // tree argmin over the NW warp winners (index only), then one read
     u32 bi = 0;
@@ -240,6 +251,27 @@ DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u
       atomicAdd(&g_xprof[1], (unsigned long long)(xc - xb));
       atomicAdd(&g_xprof[2], (unsigned long long)(xd - xc));
       atomicAdd(&g_xprof[3], 1ull);
+      if (tid == 0) {  // skew: last - first arrival, release latency, which warp was last
+        long long mx = S.xarr[par][0], mn = mx;
+        int lw = 0;
+        for (int i = 1; i < NW; ++i) {
+          const long long a = S.xarr[par][i];
+          if (a > mx) mx = a, lw = i;
+          mn = a < mn ? a : mn;
+        }
+        atomicAdd(&g_xprof[4], (unsigned long long)(mx - mn));
+        atomicAdd(&g_xprof[5], (unsigned long long)(xc - mx));
+        atomicAdd(&g_xprof[6], 1ull);
+        atomicAdd(&g_xprof[8 + lw], 1ull);
+        if (mx - mn > 1000) atomicAdd(&g_xprof[7], 1ull);
+        // phase excess of the last warp over the mean of the others
+        for (int ph = 0; ph < 8; ++ph) {
+          long long o = 0;
+          for (int i = 0; i < NW; ++i)
+            if (i != lw) o += S.xph[par][i][ph];
+          atomicAdd(&g_xprof2[ph], (unsigned long long)(S.xph[par][lw][ph] - o / (NW - 1)));
+        }
+      }
     }
 #endif
     return r;
@@ -587,8 +619,246 @@ __global__ void __launch_bounds__(32 * NW, 1)
 #define SPROF(i)
   prof = nullptr;
 #endif
+#if defined(PBH_XPROF) && defined(PBH_PROF_BUILD)
+  u64 xsnap[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+  // One pass over the edges (uu, ww)[t], t < PE, of the extracted vertex v
+  // (priority p): gather the index entries, run the deferred rescans, apply
+  // the improving candidates in place / into a new slot / into the push
+  // buffer, and exchange the offers. Shared by the steady-state loop and the
+  // general round below.
+  bool pf_has = false;  // a first-sighted vertex's row to pull into L2
+  u64 pf_b = 0, pf_e = 0;
+  auto relax_pass = [&](const u32 (&uu)[PE], const u32 (&ww)[PE], u32 rem, u32 te, u64 p,
+                        u32 v) -> BankOffer {
+    ulonglong2 ee[PE];
+    u64 ob[PE], oe[PE];
+#pragma unroll
+    for (u32 t = 0; t < PE; ++t) {
+      ee[t] = make_ulonglong2(~0ull, PBH_ST_DEAD);
+      ob[t] = oe[t] = 0;
+      if (te + B * t < rem) {
+        ee[t] = __ldca(reinterpret_cast<const ulonglong2*>(idx + uu[t]));  // L1: sole writer is this CTA
+        ob[t] = __ldg(off + uu[t]);
+        oe[t] = __ldg(off + uu[t] + 1);
+      }
+    }
+    asm volatile("" ::: "memory");  // issue the gathers before the rescans' shared loads
+#ifdef PBH_XPROF
+    if (prof) {  // split: gather latency (idx + off) | rescans
+      u32 sink = 0;
+#pragma unroll
+      for (u32 t = 0; t < PE; ++t) sink += (u32)ee[t].y + (u32)ob[t] + (u32)oe[t];
+      asm volatile("" ::"r"(sink));
+    }
+    SPROF(3);
+#endif
+    // deferred rescans (extraction owner, decreased banks) under the gathers
+    if (rescan_due) bank_rescan<B, KI>(L, tid, occm, lhas, lmin_p, lmin_k, lmin_s);
+    rescan_due = false;
+#ifdef PBH_PROF_BUILD
+    if (prof) {
+      u32 sink = 0;
+#pragma unroll
+      for (u32 t = 0; t < PE; ++t) sink += (u32)ee[t].y;
+      asm volatile("" ::"r"(sink));
+    }
+#endif
+#ifdef PBH_XPROF
+    SPROF(7);
+#else
+    SPROF(3);
+#endif
+    // ---- candidates, applied by the relaxing thread
+    u32 fresh = 0, nimp = 0, nq = 0;
+    bool ovf = false, bad = false;
+    pf_has = false;
+    bool ch = false;
+    u64 cbp = 0, cbrb = 0;
+    u32 cbk = 0, cbs = 0, cbd = 0;
+#pragma unroll
+    for (u32 t = 0; t < PE; ++t) {
+      const u32 st = (u32)ee[t].y;
+      const u64 c = p + ww[t];
+      if (!(te + B * t < rem) || (!dag_mode && PBH_ST(st) == PBH_ST_DEAD)) continue;
+      ovf |= c < p;
+      if (!(c < ee[t].x)) continue;
+      const u32 u = uu[t];
+      ++nimp;
+      fresh += PBH_ST(st) != PBH_ST_LIVE;
+      const u32 loc = st >> 2;
+      u32 nst, sl = 0;
+      bool admitted = true;
+      if (PBH_ST(st) == PBH_ST_LIVE && loc < C0) {
+        // decrease in place; the owner rescans next pass
+        bad |= !(L.lk[loc] == u && L.lp[loc] == ee[t].x);
+        L.lp[loc] = c;
+        S.dirty[par][loc % B] = 1;
+        nst = st;
+        sl = loc;
+      } else if (L.spl_inf || c < L.spl_p || (c == L.spl_p && u <= L.spl_k)) {
+        const u32 i = __ffs(~occm) - 1;
+        sl = i * B + tid;
+        occm |= 1u << i;
+        L.lk[sl] = u;
+        L.lp[sl] = c;
+        L.lrb[sl] = ob[t];
+        L.ldeg[sl] = (u32)(oe[t] - ob[t]);
+        if (!lhas || less_pk(c, u, lmin_p, lmin_k)) {
+          lhas = true;
+          lmin_p = c;
+          lmin_k = u;
+          lmin_s = sl;
+        }
+        nst = PBH_ST_LIVE | (sl << 2);
+        if (PBH_ST(st) != PBH_ST_LIVE) {
+          // first sighting of a vertex that may be extracted soon: its row is
+          // pulled into L2 after the exchange (warp-cooperatively; a second
+          // fresh row in the same pass falls back to the bulk prefetch)
+          if (pf_has) {
+            l2_prefetch_range(tgt, pf_b, pf_e);
+            l2_prefetch_range(wt, pf_b, pf_e);
+          }
+          pf_has = true;
+          pf_b = ob[t];
+          pf_e = oe[t];
+        }
+      } else {
+        const u32 qp_ = atomicAdd(&L.qn, 1u);
+        L.qk[qp_] = u;
+        L.qp[qp_] = c;
+        ++nq;
+        admitted = false;
+        nst = PBH_ST_LIVE | (PBH_LOC_DEEP << 2);
+      }
+      if (admitted && (!ch || less_pk(c, u, cbp, cbk))) {
+        ch = true;
+        cbp = c;
+        cbk = u;
+        cbs = sl;
+        cbrb = ob[t];
+        cbd = (u32)(oe[t] - ob[t]);
+      }
+      pbh_idx_entry e;
+      e.prio = c;
+      e.state = nst;
+      e.parent = v;
+      __stwb(reinterpret_cast<ulonglong2*>(idx) + u, *reinterpret_cast<const ulonglong2*>(&e));
+    }
+    SPROF(4);
+    // ---- exchange: this thread offers min(bank minimum, best candidate)
+    bool oh = lhas;
+    u64 op = lmin_p;
+    u32 ok = lmin_k, os = lmin_s;
+    u64 orb = cbrb;
+    u32 od = cbd;
+    if (ch && (!oh || less_pk(cbp, cbk, op, ok))) {
+      oh = true;
+      op = cbp;
+      ok = cbk;
+      os = cbs;
+    } else if (oh) {
+      orb = L.lrb[os];
+      od = L.ldeg[os];
+    }
+#if defined(PBH_XPROF) && defined(PBH_PROF_BUILD)
+    if ((tid & 31) == 0)
+      for (int i = 0; i < 8; ++i) {
+        S.xph[par][tid >> 5][i] = (long long)(pc[i] - xsnap[i]);
+        xsnap[i] = pc[i];
+      }
+#endif
+    const u32 ev = (u32)__popc(occm) > (u32)KI - PE ? 1u : 0u;
+    const BankOffer r = bank_exchange<NW, KI, VT>(
+        par, oh, op, ok, os, orb, od, fresh | (nimp << 9) | ((ovf ? 1u : 0u) << 18),
+        nq | (ev << 9) | ((bad ? 1u : 0u) << 18));
+    if (S.dirty[par][tid]) {
+      S.dirty[par][tid] = 0;
+      rescan_due = true;
+    }
+    par ^= 1;
+    live += r.fresh;
+    qn += r.nq;
+    evict_due = (r.flags & 1u) != 0;
+    return r;
+  };
+  // The next extraction is known: copy its row's first pass into S.pf (the
+  // edge j -> thread (j - rot') mod B mapping of the next round), then issue
+  // the L2 prefetches of this pass's first sightings under that copy.
+  auto next_row = [&](const BankOffer& r, u32 rot) {
+    const u32 te2 = (tid + rot + 1) & (B - 1);
+#pragma unroll
+    for (u32 t = 0; t < PE; ++t) {
+      const u32 j = te2 + B * t;
+      const bool in = j < r.deg;
+      cp_async4(&S.pf_t[t * B + tid], in ? tgt + r.rb + j : tgt, in);
+      cp_async4(&S.pf_w[t * B + tid], in ? wt + r.rb + j : wt, in);
+    }
+    cp_async_commit();
+  };
+  auto fresh_rows_l2 = [&]() {
+    for (u32 fm = __ballot_sync(0xffffffffu, pf_has); fm; fm &= fm - 1) {
+      const u32 src = __ffs(fm) - 1;
+      const u64 b = __shfl_sync(0xffffffffu, pf_b, src), e = __shfl_sync(0xffffffffu, pf_e, src);
+      l2_prefetch_rows(tgt, wt, b, e, tid & 31);
+    }
+    pf_has = false;
+  };
+  auto settle = [&](u64 p, u32 v) {
+    if (tid == 0) {
+      idx[v].state = PBH_ST_DEAD;
+      my_dist[v] = p;
+      my_settled[n_settled] = v;
+    }
+    ++n_settled;
+    ++rounds;
+    ++ops;
+    --live;
+  };
+
   u32 fail_v = 0;
   while (live > 0) {
+    // ---- steady state (most rounds): the next extraction is known, its row
+    // fits one pass (already in S.pf) and no cold work is due
+    while (nx && cur.deg <= PASS && !evict_due && qn <= (u32)(kBankQ - PASS) && grow_ok &&
+           (u64)qn + deep_n <= grow_at) {
+      const u64 p = cur.p;
+      const u32 v = cur.k;
+      if (cur.slot % B == tid) {
+        occm &= ~(1u << (cur.slot / B));
+        rescan_due = true;
+      }
+      const u32 rot = (u32)n_settled & (B - 1);
+      const u32 te = (tid + rot) & (B - 1);
+      settle(p, v);
+      SPROF(0);
+      u32 uu[PE], ww[PE];
+      cp_async_wait_all();
+#pragma unroll
+      for (u32 t = 0; t < PE; ++t) {
+        uu[t] = S.pf_t[t * B + tid];
+        ww[t] = S.pf_w[t * B + tid];
+      }
+      SPROF(2);
+      const BankOffer r = relax_pass(uu, ww, cur.deg, te, p, v);
+      if (r.flags & 6u) {
+        fail_bad = (r.flags & 2u) != 0;
+        fail_ovf = (r.flags & 4u) != 0;
+        fail_v = v;
+        break;
+      }
+      SPROF(5);
+      nx = r.has;
+      if (r.has) {
+        cur = r;
+        next_row(r, rot);
+      }
+      fresh_rows_l2();
+      if (r.nimp) ops += r.nimp <= d ? 1u : ceil_div_cold(r.nimp, d);
+      SPROF(6);
+    }
+    if (fail_bad || fail_ovf || live <= 0) break;
+    // ---- general round
     if (!grow_ok || (u64)qn + deep_n > grow_at) {
       need_grow = true;
       break;
@@ -623,15 +893,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
       rescan_due = true;
     }
     const u32 rot = (u32)n_settled & (B - 1);  // edge j of a pass -> thread (j - rot) mod B
-    if (tid == 0) {
-      idx[v].state = PBH_ST_DEAD;
-      my_dist[v] = p;
-      my_settled[n_settled] = v;
-    }
-    ++n_settled;
-    ++rounds;
-    ++ops;
-    --live;
+    settle(p, v);
     // ---- relax the row in passes of 256 edges (sssp.cpp:49-57)
     u32 n_imp = 0;
     const u64 rb = cur.rb;
@@ -671,138 +933,17 @@ __global__ void __launch_bounds__(32 * NW, 1)
           ww[t] = in ? __ldg(wt + base + te + B * t) : 0;
         }
       }
-      ulonglong2 ee[PE];
-      u64 ob[PE], oe[PE];
 #ifdef PBH_PROF_BUILD
       if (prof) {  // make the row load visible in its own bucket
         u32 sink = 0;
 #pragma unroll
         for (u32 t = 0; t < PE; ++t) sink += uu[t];
-        if (sink == 0xfffffffeu) pc[7] += 1;
+        asm volatile("" ::"r"(sink));
       }
 #endif
       SPROF(2);
-#pragma unroll
-      for (u32 t = 0; t < PE; ++t) {
-        ee[t] = make_ulonglong2(~0ull, PBH_ST_DEAD);
-        ob[t] = oe[t] = 0;
-        if (te + B * t < rem) {
-          ee[t] = __ldca(reinterpret_cast<const ulonglong2*>(idx + uu[t]));  // L1: sole writer is this CTA
-          ob[t] = __ldg(off + uu[t]);
-          oe[t] = __ldg(off + uu[t] + 1);
-        }
-      }
-      asm volatile("" ::: "memory");  // issue the gathers before the rescans' shared loads
-      // deferred rescans (extraction owner, decreased banks) under the gathers
-      if (rescan_due) bank_rescan<B, KI>(L, tid, occm, lhas, lmin_p, lmin_k, lmin_s);
-      rescan_due = false;
-      // ---- candidates, applied by the relaxing thread
-#ifdef PBH_PROF_BUILD
-      if (prof) {
-        u32 sink = 0;
-#pragma unroll
-        for (u32 t = 0; t < PE; ++t) sink += (u32)ee[t].y;
-        if (sink == 0xfffffffeu) pc[7] += 1;
-      }
-#endif
-      SPROF(3);
-      u32 fresh = 0, nimp = 0, nq = 0;
-      bool ovf = false, bad = false;
-      bool ch = false;
-      u64 cbp = 0, cbrb = 0;
-      u32 cbk = 0, cbs = 0, cbd = 0;
-#pragma unroll
-      for (u32 t = 0; t < PE; ++t) {
-        const u32 st = (u32)ee[t].y;
-        const u64 c = p + ww[t];
-        if (!(te + B * t < rem) || (!dag_mode && PBH_ST(st) == PBH_ST_DEAD)) continue;
-        ovf |= c < p;
-        if (!(c < ee[t].x)) continue;
-        const u32 u = uu[t];
-        ++nimp;
-        fresh += PBH_ST(st) != PBH_ST_LIVE;
-        const u32 loc = st >> 2;
-        u32 nst, sl = 0;
-        bool admitted = true;
-        if (PBH_ST(st) == PBH_ST_LIVE && loc < C0) {
-          // decrease in place; the owner rescans next pass
-          bad |= !(L.lk[loc] == u && L.lp[loc] == ee[t].x);
-          L.lp[loc] = c;
-          S.dirty[par][loc % B] = 1;
-          nst = st;
-          sl = loc;
-        } else if (L.spl_inf || c < L.spl_p || (c == L.spl_p && u <= L.spl_k)) {
-          const u32 i = __ffs(~occm) - 1;
-          sl = i * B + tid;
-          occm |= 1u << i;
-          L.lk[sl] = u;
-          L.lp[sl] = c;
-          L.lrb[sl] = ob[t];
-          L.ldeg[sl] = (u32)(oe[t] - ob[t]);
-          if (!lhas || less_pk(c, u, lmin_p, lmin_k)) {
-            lhas = true;
-            lmin_p = c;
-            lmin_k = u;
-            lmin_s = sl;
-          }
-          nst = PBH_ST_LIVE | (sl << 2);
-          if (PBH_ST(st) != PBH_ST_LIVE) {
-            // first sighting of a vertex that may be extracted soon: pull its
-            // row into L2 so its first pass loads at L2 latency
-            l2_prefetch_range(tgt, ob[t], oe[t]);
-            l2_prefetch_range(wt, ob[t], oe[t]);
-          }
-        } else {
-          const u32 qp_ = atomicAdd(&L.qn, 1u);
-          L.qk[qp_] = u;
-          L.qp[qp_] = c;
-          ++nq;
-          admitted = false;
-          nst = PBH_ST_LIVE | (PBH_LOC_DEEP << 2);
-        }
-        if (admitted && (!ch || less_pk(c, u, cbp, cbk))) {
-          ch = true;
-          cbp = c;
-          cbk = u;
-          cbs = sl;
-          cbrb = ob[t];
-          cbd = (u32)(oe[t] - ob[t]);
-        }
-        pbh_idx_entry e;
-        e.prio = c;
-        e.state = nst;
-        e.parent = v;
-        reinterpret_cast<ulonglong2*>(idx)[u] = *reinterpret_cast<const ulonglong2*>(&e);
-      }
-      SPROF(4);
-      // ---- exchange: this thread offers min(bank minimum, best candidate)
-      bool oh = lhas;
-      u64 op = lmin_p;
-      u32 ok = lmin_k, os = lmin_s;
-      u64 orb = cbrb;
-      u32 od = cbd;
-      if (ch && (!oh || less_pk(cbp, cbk, op, ok))) {
-        oh = true;
-        op = cbp;
-        ok = cbk;
-        os = cbs;
-      } else if (oh) {
-        orb = L.lrb[os];
-        od = L.ldeg[os];
-      }
-      const u32 ev = (u32)__popc(occm) > (u32)KI - PE ? 1u : 0u;
-      const BankOffer r = bank_exchange<NW, KI, VT>(
-          par, oh, op, ok, os, orb, od, fresh | (nimp << 9) | ((ovf ? 1u : 0u) << 18),
-          nq | (ev << 9) | ((bad ? 1u : 0u) << 18));
-      if (S.dirty[par][tid]) {
-        S.dirty[par][tid] = 0;
-        rescan_due = true;
-      }
-      par ^= 1;
+      const BankOffer r = relax_pass(uu, ww, rem, te, p, v);
       n_imp += r.nimp;
-      live += r.fresh;
-      qn += r.nq;
-      evict_due = (r.flags & 1u) != 0;
       if (r.flags & 6u) {
         fail_bad = (r.flags & 2u) != 0;
         fail_ovf = (r.flags & 4u) != 0;
@@ -814,16 +955,9 @@ __global__ void __launch_bounds__(32 * NW, 1)
         // the next extraction: load its row's first pass now
         nx = true;
         cur = r;
-        const u32 te2 = (tid + rot + 1) & (B - 1);
-#pragma unroll
-        for (u32 t = 0; t < PE; ++t) {
-          const u32 j = te2 + B * t;
-          const bool in = j < r.deg;
-          cp_async4(&S.pf_t[t * B + tid], in ? tgt + r.rb + j : tgt, in);
-          cp_async4(&S.pf_w[t * B + tid], in ? wt + r.rb + j : wt, in);
-        }
-        cp_async_commit();
+        next_row(r, rot);
       }
+      fresh_rows_l2();
     }
     SPROF(6);
     if (cold_fail || fail_bad || fail_ovf) break;

@@ -62,6 +62,15 @@ DEV void cp_async4(void* smem, const void* gmem, bool pred) {
                "r"(pred ? 4 : 0)
                : "memory");
 }
+// Warp-cooperative L2 prefetch of the first 2 KB of two 4-byte arrays over
+// [i0, i1): lanes 0-15 take the lines of a, lanes 16-31 those of b, one
+// prefetch.global.L2 each (no uniform operands, so no divergent waterfall).
+DEV void l2_prefetch_rows(const u32* a, const u32* b, u64 i0, u64 i1, u32 lane) {
+  const u32* arr = lane < 16 ? a : b;
+  const u64 lo = reinterpret_cast<u64>(arr + i0), hi = reinterpret_cast<u64>(arr + i1);
+  const u64 line = (lo & ~127ull) + (u64)(lane & 15) * 128;
+  if (line < hi) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(line));
+}
 // Bulk L2 prefetch of the 4-byte array range [a[i0], a[i1]) (16-byte granular).
 DEV void l2_prefetch_range(const u32* a, u64 i0, u64 i1) {
   const u64 b0 = (reinterpret_cast<u64>(a + i0)) & ~15ull;

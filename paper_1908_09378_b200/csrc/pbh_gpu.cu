@@ -282,8 +282,18 @@ cudaError_t launch_sssp_bank(cudaStream_t st, u32 grid, pbh_heap_dev* heaps, con
     cudaMemcpy(pc, prof, 64 * 8, cudaMemcpyDeviceToHost);
     cudaMemset(prof, 0, 64 * 8);
 #ifdef PBH_XPROF
-    unsigned long long xp[8];
+    unsigned long long xp[16];
     cudaMemcpyFromSymbol(xp, g_xprof, sizeof xp);
+    if (xp[6]) fprintf(stderr, "exchange skew (block 0): last-first %.0f release %.0f  >1000cyc %.3f  last warp %llu %llu %llu %llu\n",
+                       (double)xp[4] / xp[6], (double)xp[5] / xp[6], (double)xp[7] / xp[6], xp[8], xp[9], xp[10], xp[11]);
+    unsigned long long z[16] = {}, x2[8];
+    cudaMemcpyFromSymbol(x2, g_xprof2, sizeof x2);
+    if (xp[6]) fprintf(stderr, "last warp excess per phase (top pre-row row gather apply exch tail rescan): %.0f %.0f %.0f %.0f %.0f %.0f %.0f %.0f\n",
+                       (double)(long long)x2[0] / xp[6], (double)(long long)x2[1] / xp[6], (double)(long long)x2[2] / xp[6],
+                       (double)(long long)x2[3] / xp[6], (double)(long long)x2[4] / xp[6], (double)(long long)x2[5] / xp[6],
+                       (double)(long long)x2[6] / xp[6], (double)(long long)x2[7] / xp[6]);
+    cudaMemcpyToSymbol(g_xprof, z, sizeof z);
+    cudaMemcpyToSymbol(g_xprof2, z, sizeof x2);
     if (xp[3]) fprintf(stderr, "exchange per call (warp leaders, block 0): reduce %.0f barrier %.0f combine %.0f (n=%llu)\n",
                        (double)xp[0] / xp[3], (double)xp[1] / xp[3], (double)xp[2] / xp[3], xp[3]);
 #endif
