@@ -71,6 +71,14 @@ struct BankOffer {
   u32 fresh, nimp, nq, flags;  // flags: 1 evict due, 2 bad slot, 4 overflow
 };
 
+// A warp's offer in the SSSP rounds' exchange: (p, k) = (~0, ~0) is "none";
+// the winner's row is read from its slot after the barrier.
+struct __align__(16) LeanOffer {
+  u64 p;
+  u32 k, slot;
+  u32 c0, c1, pad0, pad1;
+};
+
 template <int NW, int KI, int VT, bool MW = false>
 struct BankSmem {
   static constexpr int B = 32 * NW;
@@ -85,6 +93,7 @@ struct BankSmem {
   u32 pf_t[kBankPass];  // next row's first pass, prefetched by cp.async
   u32 pf_w[kBankPass];
   BankOffer ex[2][NW];  // per-pass exchange (parity double-buffered)
+  LeanOffer lx[2][NW];  // the SSSP rounds' lean exchange
   u8 dirty[2][B];       // decreased-bank flags (parity double-buffered)
   HeapSmem<B, VT> hs;
 #ifdef PBH_XPROF
@@ -276,6 +285,63 @@ DEV BankOffer bank_exchange(u32 par, bool has, u64 p, u32 k, u32 slot, u64 rb, u
 #endif
     return r;
   }
+}
+
+// Lean per-pass exchange of the SSSP rounds: CTA argmin of (p, k) with the
+// offering slot, plus the packed counter sums (see bank_exchange). Absent
+// offers are (~0, ~0). Branch-free combine of the NW warp winners.
+struct LeanRes {
+  u64 p;
+  u32 k, slot;
+  bool has;
+  u32 fresh, nimp, nq, flags;
+};
+template <int NW, int KI, int VT>
+DEV LeanRes lean_exchange(u32 par, u64 p, u32 k, u32 slot, u32 c0, u32 c1) {
+  BankSmem<NW, KI, VT>& S = bank_smem<NW, KI, VT>();
+  const u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const u32 hi = (u32)(p >> 32);
+  const u32 mhi = __reduce_min_sync(0xffffffffu, hi);
+  const bool e1 = hi == mhi;
+  const u32 mlo = __reduce_min_sync(0xffffffffu, e1 ? (u32)p : 0xffffffffu);
+  const bool e2 = e1 && (u32)p == mlo;
+  const u32 mk = __reduce_min_sync(0xffffffffu, e2 ? k : 0xffffffffu);
+  const u32 win = __ballot_sync(0xffffffffu, e2 && k == mk);
+  const u32 s0 = __reduce_add_sync(0xffffffffu, c0);
+  const u32 s1 = __reduce_add_sync(0xffffffffu, c1);
+  if (lane == (u32)(__ffs(win) - 1)) {
+    LeanOffer o;
+    o.p = ((u64)mhi << 32) | mlo;
+    o.k = mk;
+    o.slot = slot;
+    o.c0 = s0;
+    o.c1 = s1;
+    o.pad0 = o.pad1 = 0;
+    S.lx[par][w] = o;
+  }
+  __syncthreads();
+  LeanOffer b = S.lx[par][0];
+  u32 t0 = b.c0, t1 = b.c1;
+#pragma unroll
+  for (int i = 1; i < NW; ++i) {
+    const LeanOffer x = S.lx[par][i];
+    t0 += x.c0;
+    t1 += x.c1;
+    const bool lt = x.p < b.p || (x.p == b.p && x.k < b.k);
+    b.p = lt ? x.p : b.p;
+    b.k = lt ? x.k : b.k;
+    b.slot = lt ? x.slot : b.slot;
+  }
+  LeanRes r;
+  r.p = b.p;
+  r.k = b.k;
+  r.slot = b.slot;
+  r.has = !(b.p == ~0ull && b.k == 0xffffffffu);
+  r.fresh = t0 & 511u;
+  r.nimp = (t0 >> 9) & 511u;
+  r.nq = t1 & 511u;
+  r.flags = ((t1 >> 9) & 511u ? 1u : 0u) | ((t1 >> 18) & 511u ? 2u : 0u) | ((t0 >> 18) & 511u ? 4u : 0u);
+  return r;
 }
 
 template <int NW, int KI, int VT, bool MW = false>
@@ -602,7 +668,18 @@ __global__ void __launch_bounds__(32 * NW, 1)
   // replicated: some bank lacks room for a pass (also after a resume)
   bool evict_due = Bk::any(__popc(occm) > (int)(KI - PE), hc.scr());
   bool nx = false;            // the next extraction is known (cur)
-  BankOffer cur{};
+  struct {
+    u64 p, rb;
+    u32 k, slot, deg;
+  } cur{};
+  // the extraction's row from its slot (written before the exchange barrier)
+  auto take = [&](const LeanRes& r) {
+    cur.p = r.p;
+    cur.k = r.k;
+    cur.slot = r.slot;
+    cur.rb = L.lrb[r.slot];
+    cur.deg = L.ldeg[r.slot];
+  };
   bool fail_bad = false, fail_ovf = false;
   // round-phase breakdown per warp (build with -DPBH_PROF_BUILD, run with
   // PBH_PHASES=1); compiled out otherwise (it costs ~7 % of a round)
@@ -630,7 +707,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
   bool pf_has = false;  // a first-sighted vertex's row to pull into L2
   u64 pf_b = 0, pf_e = 0;
   auto relax_pass = [&](const u32 (&uu)[PE], const u32 (&ww)[PE], u32 rem, u32 te, u64 p,
-                        u32 v) -> BankOffer {
+                        u32 v) -> LeanRes {
     ulonglong2 ee[PE];
     u64 ob[PE], oe[PE];
 #pragma unroll
@@ -673,9 +750,9 @@ __global__ void __launch_bounds__(32 * NW, 1)
     u32 fresh = 0, nimp = 0, nq = 0;
     bool ovf = false, bad = false;
     pf_has = false;
-    bool ch = false;
-    u64 cbp = 0, cbrb = 0;
-    u32 cbk = 0, cbs = 0, cbd = 0;
+    // this thread's offer: min(bank minimum, best admitted candidate)
+    u64 op = lhas ? lmin_p : ~0ull;
+    u32 ok = lhas ? lmin_k : 0xffffffffu, os = lmin_s;
 #pragma unroll
     for (u32 t = 0; t < PE; ++t) {
       const u32 st = (u32)ee[t].y;
@@ -731,13 +808,10 @@ __global__ void __launch_bounds__(32 * NW, 1)
         admitted = false;
         nst = PBH_ST_LIVE | (PBH_LOC_DEEP << 2);
       }
-      if (admitted && (!ch || less_pk(c, u, cbp, cbk))) {
-        ch = true;
-        cbp = c;
-        cbk = u;
-        cbs = sl;
-        cbrb = ob[t];
-        cbd = (u32)(oe[t] - ob[t]);
+      if (admitted && less_pk(c, u, op, ok)) {
+        op = c;
+        ok = u;
+        os = sl;
       }
       pbh_idx_entry e;
       e.prio = c;
@@ -746,21 +820,6 @@ __global__ void __launch_bounds__(32 * NW, 1)
       __stwb(reinterpret_cast<ulonglong2*>(idx) + u, *reinterpret_cast<const ulonglong2*>(&e));
     }
     SPROF(4);
-    // ---- exchange: this thread offers min(bank minimum, best candidate)
-    bool oh = lhas;
-    u64 op = lmin_p;
-    u32 ok = lmin_k, os = lmin_s;
-    u64 orb = cbrb;
-    u32 od = cbd;
-    if (ch && (!oh || less_pk(cbp, cbk, op, ok))) {
-      oh = true;
-      op = cbp;
-      ok = cbk;
-      os = cbs;
-    } else if (oh) {
-      orb = L.lrb[os];
-      od = L.ldeg[os];
-    }
 #if defined(PBH_XPROF) && defined(PBH_PROF_BUILD)
     if ((tid & 31) == 0)
       for (int i = 0; i < 8; ++i) {
@@ -769,9 +828,9 @@ __global__ void __launch_bounds__(32 * NW, 1)
       }
 #endif
     const u32 ev = (u32)__popc(occm) > (u32)KI - PE ? 1u : 0u;
-    const BankOffer r = bank_exchange<NW, KI, VT>(
-        par, oh, op, ok, os, orb, od, fresh | (nimp << 9) | ((ovf ? 1u : 0u) << 18),
-        nq | (ev << 9) | ((bad ? 1u : 0u) << 18));
+    const LeanRes r = lean_exchange<NW, KI, VT>(par, op, ok, os,
+                                                fresh | (nimp << 9) | ((ovf ? 1u : 0u) << 18),
+                                                nq | (ev << 9) | ((bad ? 1u : 0u) << 18));
     if (S.dirty[par][tid]) {
       S.dirty[par][tid] = 0;
       rescan_due = true;
@@ -785,14 +844,14 @@ __global__ void __launch_bounds__(32 * NW, 1)
   // The next extraction is known: copy its row's first pass into S.pf (the
   // edge j -> thread (j - rot') mod B mapping of the next round), then issue
   // the L2 prefetches of this pass's first sightings under that copy.
-  auto next_row = [&](const BankOffer& r, u32 rot) {
+  auto next_row = [&](u32 rot) {
     const u32 te2 = (tid + rot + 1) & (B - 1);
 #pragma unroll
     for (u32 t = 0; t < PE; ++t) {
       const u32 j = te2 + B * t;
-      const bool in = j < r.deg;
-      cp_async4(&S.pf_t[t * B + tid], in ? tgt + r.rb + j : tgt, in);
-      cp_async4(&S.pf_w[t * B + tid], in ? wt + r.rb + j : wt, in);
+      const bool in = j < cur.deg;
+      cp_async4(&S.pf_t[t * B + tid], in ? tgt + cur.rb + j : tgt, in);
+      cp_async4(&S.pf_w[t * B + tid], in ? wt + cur.rb + j : wt, in);
     }
     cp_async_commit();
   };
@@ -840,7 +899,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
         ww[t] = S.pf_w[t * B + tid];
       }
       SPROF(2);
-      const BankOffer r = relax_pass(uu, ww, cur.deg, te, p, v);
+      const LeanRes r = relax_pass(uu, ww, cur.deg, te, p, v);
       if (r.flags & 6u) {
         fail_bad = (r.flags & 2u) != 0;
         fail_ovf = (r.flags & 4u) != 0;
@@ -850,8 +909,8 @@ __global__ void __launch_bounds__(32 * NW, 1)
       SPROF(5);
       nx = r.has;
       if (r.has) {
-        cur = r;
-        next_row(r, rot);
+        take(r);
+        next_row(rot);
       }
       fresh_rows_l2();
       if (r.nimp) ops += r.nimp <= d ? 1u : ceil_div_cold(r.nimp, d);
@@ -868,10 +927,11 @@ __global__ void __launch_bounds__(32 * NW, 1)
       // ---- extract_min: CTA argmin of the bank minima
       if (rescan_due) bank_rescan<B, KI>(L, tid, occm, lhas, lmin_p, lmin_k, lmin_s);
       rescan_due = false;
-      cur = bank_exchange<NW, KI, VT>(par, lhas, lmin_p, lmin_k, lmin_s,
-                                      lhas ? L.lrb[lmin_s] : 0, lhas ? L.ldeg[lmin_s] : 0, 0, 0);
+      const LeanRes x = lean_exchange<NW, KI, VT>(par, lhas ? lmin_p : ~0ull,
+                                                  lhas ? lmin_k : 0xffffffffu, lmin_s, 0, 0);
       par ^= 1;
-      if (!cur.has) {
+      if (x.has) take(x);
+      if (!x.has) {
         BANK_TO_H();
         H.refill();
         BANK_FROM_H();
@@ -942,7 +1002,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
       }
 #endif
       SPROF(2);
-      const BankOffer r = relax_pass(uu, ww, rem, te, p, v);
+      const LeanRes r = relax_pass(uu, ww, rem, te, p, v);
       n_imp += r.nimp;
       if (r.flags & 6u) {
         fail_bad = (r.flags & 2u) != 0;
@@ -954,8 +1014,8 @@ __global__ void __launch_bounds__(32 * NW, 1)
       if (last && r.has) {
         // the next extraction: load its row's first pass now
         nx = true;
-        cur = r;
-        next_row(r, rot);
+        take(r);
+        next_row(rot);
       }
       fresh_rows_l2();
     }
