@@ -706,13 +706,14 @@ __global__ void __launch_bounds__(32 * NW, 1)
   // general round below.
   bool pf_has = false;  // a first-sighted vertex's row to pull into L2
   u64 pf_b = 0, pf_e = 0;
+  const bool dag = dag_mode != 0;
   auto relax_pass = [&](const u32 (&uu)[PE], const u32 (&ww)[PE], u32 rem, u32 te, u64 p,
                         u32 v) -> LeanRes {
     ulonglong2 ee[PE];
     u64 ob[PE], oe[PE];
 #pragma unroll
     for (u32 t = 0; t < PE; ++t) {
-      ee[t] = make_ulonglong2(~0ull, PBH_ST_DEAD);
+      ee[t] = make_ulonglong2(0ull, PBH_ST_DEAD);  // no edge: never improves (c < 0)
       ob[t] = oe[t] = 0;
       if (te + B * t < rem) {
         ee[t] = __ldca(reinterpret_cast<const ulonglong2*>(idx + uu[t]));  // L1: sole writer is this CTA
@@ -755,11 +756,12 @@ __global__ void __launch_bounds__(32 * NW, 1)
     u32 ok = lhas ? lmin_k : 0xffffffffu, os = lmin_s;
 #pragma unroll
     for (u32 t = 0; t < PE; ++t) {
+      // (an absent edge has w = 0 and entry (0, DEAD): c = p, no overflow, no improvement)
       const u32 st = (u32)ee[t].y;
       const u64 c = p + ww[t];
-      if (!(te + B * t < rem) || (!dag_mode && PBH_ST(st) == PBH_ST_DEAD)) continue;
-      ovf |= c < p;
-      if (!(c < ee[t].x)) continue;
+      const bool open = dag | (PBH_ST(st) != PBH_ST_DEAD);
+      ovf |= open & (c < p);
+      if (!(open & (c < ee[t].x))) continue;
       const u32 u = uu[t];
       ++nimp;
       fresh += PBH_ST(st) != PBH_ST_LIVE;
@@ -879,8 +881,11 @@ __global__ void __launch_bounds__(32 * NW, 1)
   while (live > 0) {
     // ---- steady state (most rounds): the next extraction is known, its row
     // fits one pass (already in S.pf) and no cold work is due
-    while (nx && cur.deg <= PASS && !evict_due && qn <= (u32)(kBankQ - PASS) && grow_ok &&
-           (u64)qn + deep_n <= grow_at) {
+    // (qn + deep_n <= grow_at and qn <= kBankQ - PASS as one bound; deep_n
+    // only changes on the cold path)
+    const bool steady_ok = grow_ok && deep_n <= grow_at;
+    const u32 qn_cap = (u32)min((u64)(kBankQ - PASS), steady_ok ? grow_at - deep_n : (u64)0);
+    while (steady_ok && nx && cur.deg <= PASS && !evict_due && qn <= qn_cap) {
       const u64 p = cur.p;
       const u32 v = cur.k;
       if (cur.slot % B == tid) {
