@@ -672,13 +672,25 @@ __global__ void __launch_bounds__(32 * NW, 1)
     u64 p, rb;
     u32 k, slot, deg;
   } cur{};
-  // the extraction's row from its slot (written before the exchange barrier)
+  // Take the exchange winner as the next extraction: its row from its slot
+  // (written before the exchange barrier). free_cur(): the owner frees the
+  // slot and rescans its bank — at the round start, or for dense rows early,
+  // under the next row's copy (`freed`; a NEED_GROW exit before the vertex is
+  // settled re-occupies the slot).
   auto take = [&](const LeanRes& r) {
     cur.p = r.p;
     cur.k = r.k;
     cur.slot = r.slot;
     cur.rb = L.lrb[r.slot];
     cur.deg = L.ldeg[r.slot];
+  };
+  bool freed = false;  // the taken extraction's slot is already freed
+  auto free_cur = [&]() {
+    if (!freed && cur.slot % B == tid) {
+      occm &= ~(1u << (cur.slot / B));
+      rescan_due = true;
+    }
+    freed = false;
   };
   bool fail_bad = false, fail_ovf = false;
   // round-phase breakdown per warp (build with -DPBH_PROF_BUILD, run with
@@ -888,10 +900,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
     while (steady_ok && nx && cur.deg <= PASS && !evict_due && qn <= qn_cap) {
       const u64 p = cur.p;
       const u32 v = cur.k;
-      if (cur.slot % B == tid) {
-        occm &= ~(1u << (cur.slot / B));
-        rescan_due = true;
-      }
+      free_cur();
       const u32 rot = (u32)n_settled & (B - 1);
       const u32 te = (tid + rot) & (B - 1);
       settle(p, v);
@@ -917,6 +926,15 @@ __global__ void __launch_bounds__(32 * NW, 1)
         take(r);
         next_row(rot);
       }
+      // the extraction owner's and the decreased banks' rescans: under the
+      // next row's copy when the row is dense (its index gathers then hit L1),
+      // else under the gathers (sparse rows' gathers miss L1)
+      if (r.has && cur.deg >= 64) {
+        free_cur();
+        freed = true;
+        if (rescan_due) bank_rescan<B, KI>(L, tid, occm, lhas, lmin_p, lmin_k, lmin_s);
+        rescan_due = false;
+      }
       fresh_rows_l2();
       if (r.nimp) ops += r.nimp <= d ? 1u : ceil_div_cold(r.nimp, d);
       SPROF(6);
@@ -925,6 +943,9 @@ __global__ void __launch_bounds__(32 * NW, 1)
     // ---- general round
     if (!grow_ok || (u64)qn + deep_n > grow_at) {
       need_grow = true;
+      // the taken extraction is not settled: its slot stays occupied (the
+      // relaunch rescans and extracts it again)
+      if (nx && freed && cur.slot % B == tid) occm |= 1u << (cur.slot / B);
       break;
     }
     const bool hit = nx;
@@ -953,10 +974,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
     SPROF(0);
     const u64 p = cur.p;
     const u32 v = cur.k;
-    if (cur.slot % B == tid) {
-      occm &= ~(1u << (cur.slot / B));
-      rescan_due = true;
-    }
+    free_cur();
     const u32 rot = (u32)n_settled & (B - 1);  // edge j of a pass -> thread (j - rot) mod B
     settle(p, v);
     // ---- relax the row in passes of 256 edges (sssp.cpp:49-57)
