@@ -389,7 +389,7 @@ def run_pbh(args, D):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": (traffic_ps * S if traffic_ps else None),
-                         "kernel": "k_sssp_bank<4,8,4> (one 128-thread CTA per source)",
+                         "kernel": "k_sssp_bank<4,8,4,256> (one 128-thread CTA per source)",
                          "alg_bytes_per_launch": alg_bytes_launch},
             "cpu_baseline": cpu,
             "e2e": {"value": edges_per_step_all / (e2e_max / 1e3), "unit": "edges/s",

@@ -1,4 +1,2 @@
-for v in lean2 lean5; do echo "== $v"; cp variants/lib_$v.so paper_1908_09378_b200/libpbh_gpu.so
-timeout 300 python tools/probe.py band_small band grid_small 2>&1 | grep -o '"name": "[^"]*"\|"ns_per_round": [0-9.]*' | paste - -
-done
-timeout 900 python -m pytest tests -m gpu -x -q -k "sssp or dijkstra or smoke" 2>&1 | tail -3
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_bytes.sum --clock-control none -k regex:k_sssp_bank -c 3 --csv --log-file gpurun_out/c5_dram_r2.csv python tools/probe.py band band64 > gpurun_out/c5_dram_r2.log 2>&1
+tail -3 gpurun_out/c5_dram_r2.log
