@@ -378,6 +378,7 @@ struct DevHeap {
   std::vector<void*> allocs;
   u32 bc = 0;     // batch capacity (pow2)
   u64 base1 = 0;  // level-1 bucket capacity (level i >= 1: base1 * 4^(i-1))
+  bool bank = false;  // banked level 0 (stages kBankQ-entry push runs in g_pk/g_pp)
 
   // Optional arena (one cudaMalloc for many heaps: an SSSP context holds
   // one heap per source), and a measuring mode that only sums the sizes.
@@ -438,7 +439,7 @@ pbh_status alloc_scratch(DevHeap& H, u32 bc, u32 nt, cudaStream_t strm = 0) {
   pbh_status st;
   H.bc = bc;
   // the banked engines stage push-buffer runs (kBankQ entries) in g_pk/g_pp
-  if (H.base1 == 4ull * kBankQ) bc = std::max<u32>(bc, kBankQ);
+  if (H.bank) bc = std::max<u32>(bc, kBankQ);
   if ((st = H.alloc((void**)&H.hd.g_bk, (u64)bc * 4))) return st;
   if ((st = H.alloc((void**)&H.hd.g_bp, (u64)bc * 8))) return st;
   if ((st = H.alloc((void**)&H.hd.g_pk, (u64)bc * 4))) return st;
@@ -747,6 +748,7 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
   u32 nlev = 2;
   if (h->bank) {
     // level 1 holds four push-buffer flushes, or four whole large batches
+    h->H.bank = true;
     h->H.base1 = std::max<u64>(4ull * kBankQ, 4 * std::min<u64>(d, 1ull << 26));
     while (nlev < 12 && (h->H.base1 << (2 * (nlev - 2))) < 2 * key_universe + 4 * kBankQ) ++nlev;
   }
@@ -1226,11 +1228,18 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
   // initial levels: enough for a few rows of relaxations
   u32 nlev = 2;
   while (nlev < 8 && ((u64)c->cap0 << (2 * (nlev - 1))) < 8ull * (c->max_deg + 1)) ++nlev;
+  // test knob: a smaller first deep level (entries), so that the NEED_GROW
+  // exit + relaunch path runs on small graphs
+  u64 base1 = 4ull * kBankQ;
+  if (const char* e = getenv("PBH_SSSP_BASE1")) {
+    base1 = std::max<u64>(strtoull(e, nullptr, 10), 2ull * kBankQ);
+    nlev = 2;
+  }
   size_t per_heap = 0;
   {
     DevHeap M;
     M.measure = true;
-    if (c->lane) M.base1 = 4ull * kBankQ;
+    if (c->lane) M.base1 = base1, M.bank = true;
     init_heap(M, c->d, c->cap0, bc, c->nt, std::max<u32>(c->V, 1), 0, nlev, c->d_heaps);
     per_heap = M.measured;
   }
@@ -1238,7 +1247,7 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
   if ((st = ctx_alloc(c, (void**)&arena, per_heap * max_sources))) return fail(st);
   for (u64 i = 0; i < max_sources; ++i) {
     DevHeap& H = c->heaps[i];
-    if (c->lane) H.base1 = 4ull * kBankQ;
+    if (c->lane) H.base1 = base1, H.bank = true;
     H.arena = arena + per_heap * i;
     H.arena_cap = per_heap;
     st = init_heap(H, c->d, c->cap0, bc, c->nt, std::max<u32>(c->V, 1), 0, nlev, c->d_heaps + i,

@@ -136,3 +136,21 @@ def test_golden_sssp_fixtures(pbh):
         r = pbh.par_dijkstra(g, 0, dag_mode=bool(z[name + "_dag"]))
         assert np.array_equal(r.dist, z[name + "_dist"]), name
         assert np.array_equal(r.settled_order, z[name + "_settled"]), name
+
+
+def test_need_grow_relaunch(pbh, O, monkeypatch):
+    # a small first deep level (PBH_SSSP_BASE1 test knob): these frontiers
+    # outgrow it, so the kernel exits with NEED_GROW — possibly with the next
+    # extraction already taken — and the relaunch resumes from the saved
+    # level-0 image; results stay bit-exact
+    from paper_1908_09378_b200 import _lib
+    monkeypatch.setenv("PBH_SSSP_BASE1", "8192")
+    # complete: dense rows beyond one pass; random 20k x 20: sparse rows;
+    # random 20k x 100: one-pass dense rows (the steady loop frees the next
+    # extraction's slot early and the exit must re-occupy it)
+    for g in (O.gen_complete(3000, 1000, 5), O.gen_random(20000, 400000, 1000, 4),
+              O.gen_random(20000, 2000000, 1000, 6)):
+        l0 = _lib.lib().pbh_launch_count()
+        check(pbh, O, g)
+        # more than the usual launches (kernel + parents + degree scan): relaunched
+        assert _lib.lib().pbh_launch_count() - l0 > 3
