@@ -31,79 +31,102 @@ constexpr u32 kStreamMin = 64;    // smallest merge streamed through the windows
 // network, shuffles below stride 32), then merge-path rounds (one search and
 // M/NT outputs per thread) double the run width, ping-ponging through
 // (TK, TP). Slots n.. of the padded width are (~0, ~0): they sort last.
+// Bitonic sort of R independent runs of 128 held in registers (run q / 4,
+// element (q % 4) * 32 + lane); the R networks interleave for ILP.
+template <int R>
+DEV void bitonic128(u64 (&p)[4 * R], u32 (&k)[4 * R], u32 lane) {
+#pragma unroll
+  for (u32 size = 2; size <= 128; size <<= 1) {
+#pragma unroll
+    for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= 32) {
+        const u32 rs = stride / 32;
+#pragma unroll
+        for (u32 q = 0; q < 4 * R; ++q) {
+          if ((q & 3) & rs) continue;
+          const u32 i = (q & 3) * 32 + lane;  // lower element of the pair
+          const bool up = (i & size) == 0;
+          const bool gt = less_pk(p[q | rs], k[q | rs], p[q], k[q]);
+          if (gt == up) {
+            const u64 tp = p[q];
+            p[q] = p[q | rs];
+            p[q | rs] = tp;
+            const u32 tk = k[q];
+            k[q] = k[q | rs];
+            k[q | rs] = tk;
+          }
+        }
+      } else {
+#pragma unroll
+        for (u32 q = 0; q < 4 * R; ++q) {
+          const u32 i = (q & 3) * 32 + lane;
+          const u32 ohi = __shfl_xor_sync(0xffffffffu, (u32)(p[q] >> 32), stride);
+          const u32 olo = __shfl_xor_sync(0xffffffffu, (u32)p[q], stride);
+          const u32 ok = __shfl_xor_sync(0xffffffffu, k[q], stride);
+          const u64 op = ((u64)ohi << 32) | olo;
+          const bool up = (i & size) == 0;
+          const bool lower = (lane & stride) == 0;
+          const bool other_less = less_pk(op, ok, p[q], k[q]);
+          if (lower == up ? other_less : !other_less) {
+            p[q] = op;
+            k[q] = ok;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Runs a, a + step, ... (R of them) of 128: load (padding (~0, ~0)), sort, store.
+template <int R>
+DEV void sort_runs128(u32* K, u64* P, u32 n, u32 a, u32 step, u32 lane) {
+  u64 p[4 * R];
+  u32 k[4 * R];
+#pragma unroll
+  for (u32 q = 0; q < 4 * R; ++q) {
+    const u32 i = (a + (q >> 2) * step) * 128 + (q & 3) * 32 + lane;
+    p[q] = i < n ? P[i] : ~0ull;
+    k[q] = i < n ? K[i] : 0xffffffffu;
+  }
+  bitonic128<R>(p, k, lane);
+#pragma unroll
+  for (u32 q = 0; q < 4 * R; ++q) {
+    const u32 i = (a + (q >> 2) * step) * 128 + (q & 3) * 32 + lane;
+    K[i] = k[q];
+    P[i] = p[q];
+  }
+}
+
+// Sort n entries (K, P) in shared memory by (p, k) with the whole CTA (K, P,
+// TK, TP hold the width n rounded up to a power of two >= 128): the warps
+// sort runs of 128 in registers (4 per lane, element r*32 + lane; bitonic
+// network, shuffles below stride 32), then merge-path rounds double the run
+// width, ping-ponging through (TK, TP): one search and an odd number of
+// consecutive outputs per thread (an even per-thread stride would put every
+// lane's stores in the same shared-memory bank). Slots n.. of the padded
+// width are (~0, ~0): they sort last.
 template <int NW>
 DEV void cta_sort(u32* K, u64* P, u32 n, u32* TK, u64* TP) {
   constexpr u32 NT = 32 * NW;
   const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   u32 M = 128;
   while (M < n) M <<= 1;
-  for (u32 run = w; run * 128 < M; run += NW) {
-    u64 p[4];
-    u32 k[4];
-#pragma unroll
-    for (u32 r = 0; r < 4; ++r) {
-      const u32 i = run * 128 + r * 32 + lane;
-      p[r] = i < n ? P[i] : ~0ull;
-      k[r] = i < n ? K[i] : 0xffffffffu;
-    }
-#pragma unroll
-    for (u32 size = 2; size <= 128; size <<= 1) {
-#pragma unroll
-      for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
-        if (stride >= 32) {
-          const u32 rs = stride / 32;
-#pragma unroll
-          for (u32 r = 0; r < 4; ++r) {
-            if (r & rs) continue;
-            const u32 i = r * 32 + lane;  // lower element of the pair
-            const bool up = (i & size) == 0;
-            const bool gt = less_pk(p[r | rs], k[r | rs], p[r], k[r]);
-            if (gt == up) {
-              const u64 tp = p[r];
-              p[r] = p[r | rs];
-              p[r | rs] = tp;
-              const u32 tk = k[r];
-              k[r] = k[r | rs];
-              k[r | rs] = tk;
-            }
-          }
-        } else {
-#pragma unroll
-          for (u32 r = 0; r < 4; ++r) {
-            const u32 i = r * 32 + lane;
-            const u32 ohi = __shfl_xor_sync(0xffffffffu, (u32)(p[r] >> 32), stride);
-            const u32 olo = __shfl_xor_sync(0xffffffffu, (u32)p[r], stride);
-            const u32 ok = __shfl_xor_sync(0xffffffffu, k[r], stride);
-            const u64 op = ((u64)ohi << 32) | olo;
-            const bool up = (i & size) == 0;
-            const bool lower = (lane & stride) == 0;
-            const bool other_less = less_pk(op, ok, p[r], k[r]);
-            if (lower == up ? other_less : !other_less) {
-              p[r] = op;
-              k[r] = ok;
-            }
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (u32 r = 0; r < 4; ++r) {
-      K[run * 128 + r * 32 + lane] = k[r];
-      P[run * 128 + r * 32 + lane] = p[r];
-    }
-  }
+  const u32 nruns = M / 128;
+  u32 run = w;
+  for (; run < nruns; run += NW) sort_runs128<1>(K, P, n, run, NW, lane);
   __syncthreads();
   u32* sk = K;
   u64* sp = P;
   u32* dk = TK;
   u64* dp = TP;
   for (u32 wr = 128; wr < M; wr <<= 1) {
-    // each thread merges one contiguous range of M / NT outputs (one
-    // merge-path search per round)
-    const u32 per = M / NT;  // M >= 128 and NT <= 256: per >= 1 when M >= NT
-    for (u32 o0 = tid * per; o0 < M; o0 += per * NT) {
-      const u32 base = (o0 / (2 * wr)) * 2 * wr;
-      const u32 d = o0 - base;
+    // each thread merges one contiguous range of `per` outputs, split at
+    // pair boundaries (one merge-path search per piece)
+    const u32 per = ((M + NT - 1) / NT) | 1u;
+    for (u32 o = tid * per, oend = min(o + per, M); o < oend;) {
+      const u32 base = (o / (2 * wr)) * 2 * wr;
+      const u32 cnt = min(oend, base + 2 * wr) - o;
+      const u32 d = o - base;
       const u32* ak = sk + base;
       const u64* ap = sp + base;
       const u32* bk = sk + base + wr;
@@ -119,22 +142,25 @@ DEV void cta_sort(u32* K, u64* P, u32 n, u32* TK, u64* TP) {
       u32 x = lo, y = d - lo;
       u64 xa = x < wr ? ap[x] : ~0ull, yb = y < wr ? bp[y] : ~0ull;
       u32 xk = x < wr ? ak[x] : 0xffffffffu, yk = y < wr ? bk[y] : 0xffffffffu;
-      for (u32 v = 0; v < per; ++v) {
-        const bool ta = x < wr && (y >= wr || less_pk(xa, xk, yb, yk));
-        if (ta) {
-          dk[o0 + v] = xk;
-          dp[o0 + v] = xa;
-          ++x;
-          xa = x < wr ? ap[x] : ~0ull;
-          xk = x < wr ? ak[x] : 0xffffffffu;
-        } else {
-          dk[o0 + v] = yk;
-          dp[o0 + v] = yb;
-          ++y;
-          yb = y < wr ? bp[y] : ~0ull;
-          yk = y < wr ? bk[y] : 0xffffffffu;
-        }
+      // branch-free: take the smaller head, reload only the side that advanced
+      // (an exhausted side's head is (~0, ~0) and loses every comparison
+      // against a real entry; padding entries are themselves (~0, ~0))
+      for (u32 v = 0; v < cnt; ++v) {
+        const bool ta = y >= wr || (x < wr && less_pk(xa, xk, yb, yk));
+        dk[o + v] = ta ? xk : yk;
+        dp[o + v] = ta ? xa : yb;
+        x += ta;
+        y += !ta;
+        const u32 i = ta ? x : y;
+        const bool in = i < wr;
+        const u64 np = in ? (ta ? ap : bp)[i] : ~0ull;
+        const u32 nk = in ? (ta ? ak : bk)[i] : 0xffffffffu;
+        xa = ta ? np : xa;
+        xk = ta ? nk : xk;
+        yb = ta ? yb : np;
+        yk = ta ? yk : nk;
       }
+      o += cnt;
     }
     __syncthreads();
     u32* t1 = sk;
