@@ -151,6 +151,7 @@ def c4(log2n, ds, batches_per_d):
         ms = r.metrics.wall_ms
         rec = {"config": "C4 bulkUpdate sweep", "heap_keys": n, "d": d, "batches": nb,
                "updates": len(v), "device_ms": ms, "updates_per_s": len(v) / (ms / 1e3),
+               "us_per_batch": ms * 1e3 / max(nb, 1),  # latency metric for small d
                "roofline_frac": 24 * len(v) / (ms / 1e3) / 1e9 / PEAK, "prefill_s": pre_s,
                "levels": len(r.metrics.resolves_per_level)}
         out.append(rec)

@@ -1,4 +1,2 @@
-for v in sort3 s4; do echo "== $v"; cp variants/lib_$v.so paper_1908_09378_b200/libpbh_gpu.so
-timeout 300 python tools/probe.py band_small band grid_small 2>&1 | grep -o '"name": "[^"]*"\|"ns_per_round": [0-9.]*' | paste - -
-done
-timeout 900 python -m pytest tests -m gpu -x -q -k "sssp or dijkstra or smoke" 2>&1 | tail -2
+ncu --set full --import-source on --clock-control none -k regex:k_sssp_bank -c 1 -o gpurun_out/grid5 python tools/probe.py grid_small > gpurun_out/grid5.log 2>&1
+tail -1 gpurun_out/grid5.log
