@@ -1199,9 +1199,29 @@ __global__ void __launch_bounds__(32 * NW, 1)
     pc[i] += (u64)(t1_ - pt0);            \
     pt0 = t1_;                            \
   }
+  // op headers run ahead: (kind, end) of op and op+1 are in registers when op
+  // starts and op+2's load during op, so op+1's exact element range is known
+  // and pulled into L2 (bulk prefetch) while op runs: an op's first loads no
+  // longer wait behind a dependent header load and an HBM miss
+  u64 hs_ = op < op_end ? tr.offsets[op] : 0;
+  u8 ka = op < op_end ? tr.kinds[op] : 0;
+  u64 ea = op < op_end ? tr.offsets[op + 1] : 0;
+  u8 kb = op + 1 < op_end ? tr.kinds[op + 1] : 0;
+  u64 eb = op + 1 < op_end ? tr.offsets[op + 2] : 0;
   for (; op < op_end; ++op) {
-    const u8 kind = tr.kinds[op];
-    const u64 ob = tr.offsets[op], oe = tr.offsets[op + 1];
+    const u8 kind = ka;
+    const u64 ob = hs_, oe = ea;
+    if (tid == 0 && op + 1 < op_end && eb > ea) {
+      l2_prefetch_range(tr.vals, ea, eb);
+      l2_prefetch_range(reinterpret_cast<const u32*>(tr.prios), 2 * ea, 2 * eb);
+    }
+    hs_ = ea;
+    ka = kb;
+    ea = eb;
+    if (op + 2 < op_end) {
+      kb = tr.kinds[op + 2];
+      eb = tr.offsets[op + 3];
+    }
     if (kind == 'U' || kind == 'B') {
       // ------------------------------------------------ bulk_update / update
       const u32* vals = tr.vals + ob;

@@ -1,2 +1,5 @@
-ncu --set full --import-source on --clock-control none -k regex:k_sssp_bank -c 1 -o gpurun_out/grid5 python tools/probe.py grid_small > gpurun_out/grid5.log 2>&1
-tail -1 gpurun_out/grid5.log
+for v in sort3 hdr; do echo "== $v"; cp variants/lib_$v.so paper_1908_09378_b200/libpbh_gpu.so
+timeout 600 python tools/probe_trace.py c1 2>&1 | tail -1 | cut -c1-150
+timeout 900 python tools/bench_suite.py c4 --c4-n 22 2>&1 >/dev/null | grep -o '"d": [0-9]*\|"us_per_batch": [0-9.]*' | paste - -
+done
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
