@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--sources", type=int, default=64, help="sources per GPU")
     ap.add_argument("--v", type=int, default=V_DEFAULT)
     ap.add_argument("--deg", type=int, default=DEG_DEFAULT)
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bulk", action="store_true", help="skip the C4 bulk_update leg")
     ap.add_argument("--cpu-sample-sources", type=int, default=0,
@@ -340,21 +340,32 @@ def run_pbh(args, D):
     single = {"edges_per_s": e_scanned / (ms1 / 1e3), "ms": ms1,
               "ns_per_round": ms1 * 1e6 / max(r1.rounds, 1), "rounds": r1.rounds,
               "roofline_frac": sssp_bytes(V, e_scanned, reached) / (ms1 / 1e3) / 1e9 / peak}
-    ctx.close()
 
-    # end-to-end through the public C-ABI with host buffers (CSR H2D + dist/parent
-    # D2H), the host arrays page-locked once outside the timed region
+    # end-to-end through the public C-ABI with host buffers, every step: the
+    # host CSR uploaded into the live context (pbh_sssp_ctx_load_graph, H2D),
+    # the solve, and every source's dist + parent read back (D2H). The host
+    # arrays are page-locked once outside the timed region; the context (its
+    # per-source heaps) is the long-lived serving state.
     dist = np.zeros((S, V), np.uint64)
     parent = np.zeros((S, V), np.uint32)
     pinned = (g.offsets, g.targets, g.weights, dist, parent)
     P.pin(*pinned)
+
+    def e2e_step():
+        ctx.load_graph(g)
+        ctx.run(srcs)
+        for i in range(S):
+            ctx.fetch_into(i, dist[i], parent[i])
+
+    e2e_step()  # warm-up
     e2e_ms = []
     for _ in range(args.e2e_steps):
         D.barrier()
         t = time.perf_counter()
-        P.par_dijkstra_multi(g, srcs, devices=(dev,), out=(dist, parent))
+        e2e_step()
         e2e_ms.append((time.perf_counter() - t) * 1e3)
     P.unpin(*pinned)
+    ctx.close()
     e2e_max = D.max(float(np.mean(e2e_ms)))
     e2e_ok = int(dist[0][V - 1]) == V - 1 if srcs[0] == 0 else True
     h2d = 8 * (V + 1) + 8 * E + 4 * S
@@ -394,7 +405,7 @@ def run_pbh(args, D):
             "cpu_baseline": cpu,
             "e2e": {"value": edges_per_step_all / (e2e_max / 1e3), "unit": "edges/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_max,
-                    "api": "pbh_sssp_multi (host CSR in, host dist/parent out)"},
+                    "api": "pbh_sssp_ctx_load_graph + pbh_sssp_ctx_run + pbh_sssp_ctx_fetch (host CSR in, host dist/parent out)"},
             "gpu_launches": int(launches),
             "clocks": clk,
             "single_source": single,

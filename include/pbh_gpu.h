@@ -164,6 +164,11 @@ pbh_status pbh_sssp_ctx_fetch(pbh_sssp_ctx* c, uint64_t source_slot, uint64_t* d
  * counts batches, `settled` lists vertices in batch order (sort by
  * (dist, vid) for the reference's settle order). mode 0 = par_dijkstra. */
 pbh_status pbh_sssp_ctx_set_mode(pbh_sssp_ctx* c, int mode);
+/* Re-upload a CSR of the same shape (vertex_count, edge_count and max
+ * out-degree) into a live context (host or device arrays), e.g. a serving
+ * loop that receives a new graph per request without re-allocating the
+ * per-source heaps. PRECONDITION if the shape differs. */
+pbh_status pbh_sssp_ctx_load_graph(pbh_sssp_ctx* c, const pbh_csr* g);
 pbh_status pbh_sssp_ctx_destroy(pbh_sssp_ctx* c);
 
 /* The multi-source batch of pbh_sssp_multi with the results gathered on

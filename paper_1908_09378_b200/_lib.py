@@ -59,6 +59,7 @@ SIGNATURES = {
     "pbh_distance_checksum": (C.c_uint64, [U64P, C.c_uint64]),
     "pbh_host_register": (C.c_int, [C.c_void_p, C.c_uint64]),
     "pbh_sssp_ctx_set_mode": (C.c_int, [C.c_void_p, C.c_int]),
+    "pbh_sssp_ctx_load_graph": (C.c_int, [C.c_void_p, C.c_void_p]),
     "pbh_sssp_multi_device": (C.c_int, [C.POINTER(Csr), U32P, C.c_uint64, C.c_uint64,
                                         C.POINTER(C.c_int), C.c_int, C.c_void_p, C.c_void_p,
                                         C.POINTER(C.c_double)]),

@@ -1125,6 +1125,7 @@ struct pbh_sssp_ctx {
   bool multi = false;  // threshold multi-extraction (pbh_sssp_ctx_set_mode)
   u32* d_mwo = nullptr;
   u32* d_mwi = nullptr;
+  unsigned long long* d_md = nullptr;  // max out-degree scratch
   std::vector<DevHeap> heaps;
   pbh_heap_dev* d_heaps = nullptr;
   SsspState* d_sst = nullptr;
@@ -1187,7 +1188,7 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
       (c->E && cudaMemcpyAsync(c->d_w, g->weights, c->E * 4, cudaMemcpyDefault, c->stream)))
     return fail(set_err(PBH_CUDA, "CSR upload failed"));
   // max out-degree on the device (graphs.cpp:47-53)
-  unsigned long long* d_md = nullptr;
+  unsigned long long*& d_md = c->d_md;
   if ((st = ctx_alloc(c, (void**)&d_md, 8))) return fail(st);
   cudaMemsetAsync(d_md, 0, 8, c->stream);
   k_max_degree<<<std::max<u32>(1, std::min<u32>(1184, (c->V + 255) / 256)), 256, 0, c->stream>>>(
@@ -1410,6 +1411,39 @@ pbh_status pbh_sssp_ctx_set_mode(pbh_sssp_ctx* c, int mode) {
     CK(cudaStreamSynchronize(c->stream));
   }
   c->multi = mode == 1;
+  return PBH_OK;
+}
+
+pbh_status pbh_sssp_ctx_load_graph(pbh_sssp_ctx* c, const pbh_csr* g) {
+  if (!c || !g) return set_err(PBH_PRECONDITION, "bad arguments");
+  if (g->vertex_count != c->V || g->edge_count != c->E)
+    return set_err(PBH_PRECONDITION, "load_graph: vertex/edge count differs from the context");
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(c->d_off, g->offsets, ((u64)c->V + 1) * 8, cudaMemcpyDefault, c->stream));
+  if (c->E) {
+    CK(cudaMemcpyAsync(c->d_tgt, g->targets, c->E * 4, cudaMemcpyDefault, c->stream));
+    CK(cudaMemcpyAsync(c->d_w, g->weights, c->E * 4, cudaMemcpyDefault, c->stream));
+  }
+  // the derived heap shapes depend on the max out-degree (sssp.cpp:24-26)
+  CK(cudaMemsetAsync(c->d_md, 0, 8, c->stream));
+  k_max_degree<<<std::max<u32>(1, std::min<u32>(1184, (c->V + 255) / 256)), 256, 0, c->stream>>>(
+      c->d_off, c->V, c->d_md);
+  g_launches++;
+  unsigned long long md = 0;
+  CK(cudaMemcpyAsync(&md, c->d_md, 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if ((u32)md != c->max_deg)
+    return set_err(PBH_PRECONDITION, "load_graph: max out-degree differs from the context");
+  if (c->d_mwo) {  // threshold mode's per-vertex minimum weights
+    CK(cudaMemsetAsync(c->d_mwi, 0xff, (u64)c->V * 4, c->stream));
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    k_min_weights<<<sms * 8, 256, 0, c->stream>>>(c->d_off, c->d_tgt, c->d_w, c->V, c->d_mwo,
+                                                  c->d_mwi);
+    g_launches++;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+  }
   return PBH_OK;
 }
 

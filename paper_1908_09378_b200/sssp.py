@@ -150,6 +150,22 @@ class SsspContext:
         raise_for(_lib.lib().pbh_sssp_ctx_set_mode(self._h, {"exact": 0, "threshold": 1}[mode]))
         self.mode = mode
 
+    def load_graph(self, g):
+        """Re-upload a same-shape CSR (host arrays: H2D; a DeviceCsr: D2D)
+        into this context (pbh_sssp_ctx_load_graph)."""
+        g = g if hasattr(g, "data_ptr") or type(g).__name__ == "DeviceCsr" else CsrGraph.of(g)
+        cs = g.c_struct()
+        raise_for(_lib.lib().pbh_sssp_ctx_load_graph(self._h, C.byref(cs)))
+        self.g = g
+
+    def fetch_into(self, slot, dist, parent=None):
+        """D2H of one source's dist (u64[V]) and parent (u32[V]) into
+        caller-owned (e.g. page-locked) arrays."""
+        raise_for(_lib.lib().pbh_sssp_ctx_fetch(
+            self._h, slot, dist.ctypes.data_as(_lib.U64P),
+            parent.ctypes.data_as(_lib.U32P) if parent is not None else None, None, None, None,
+            None))
+
     def run(self, sources, dag_mode=False) -> float:
         src = np.ascontiguousarray(sources, dtype=np.uint32)
         ms = C.c_double()

@@ -154,3 +154,28 @@ def test_need_grow_relaunch(pbh, O, monkeypatch):
         check(pbh, O, g)
         # more than the usual launches (kernel + parents + degree scan): relaunched
         assert _lib.lib().pbh_launch_count() - l0 > 3
+
+
+def test_ctx_load_graph(pbh, O):
+    # a live context re-fed a same-shape graph (new weights) solves it exactly;
+    # a different shape is a PreconditionError
+    g1 = O.gen_band(4096, 64, 2)
+    g2 = O.gen_band(4096, 64, 7)
+    ctx = pbh.SsspContext(g1, max_sources=2)
+    try:
+        for g in (g1, g2, g1):
+            ctx.load_graph(g)
+            ctx.run([0, 17])
+            for slot, s in enumerate((0, 17)):
+                want = O.dijkstra(g, s)
+                r = ctx.fetch(slot)
+                assert np.array_equal(r.dist, want["dist"])
+                assert np.array_equal(r.settled_order, want["settled_order"])
+                d = np.zeros(4096, np.uint64)
+                p = np.zeros(4096, np.uint32)
+                ctx.fetch_into(slot, d, p)
+                assert np.array_equal(d, want["dist"]) and np.array_equal(p, r.parent)
+        with pytest.raises(pbh.PreconditionError):
+            ctx.load_graph(O.gen_band(2048, 64, 2))
+    finally:
+        ctx.close()

@@ -1,6 +1,2 @@
-for v in hdr nv; do echo "== $v"; cp variants/lib_$v.so paper_1908_09378_b200/libpbh_gpu.so
-timeout 600 python tools/probe_trace.py c1 2>&1 | tail -1 | cut -c1-150
-timeout 900 python tools/bench_suite.py c4 --c4-n 22 2>&1 >/dev/null | grep -o '"d": [0-9]*\|"us_per_batch": [0-9.]*' | paste - -
-done
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_sssp_gpu.py -x -q 2>&1 | tail -3
+timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; tail -c 200 gpurun_out/bench_final.json; tail -3 gpurun_out/bench_final.err
