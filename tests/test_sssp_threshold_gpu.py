@@ -62,3 +62,11 @@ def test_band(pbh, O):
 def test_overflow_pushes_and_refills(pbh, O):
     # a wide graph: level 0 overflows into the push buffer and deeper levels
     check(pbh, O, O.gen_random(60000, 600000, 1 << 20, 9))
+
+
+def test_need_grow_relaunch(pbh, O, monkeypatch):
+    # small first deep level (PBH_SSSP_BASE1 test knob): the threshold engine
+    # exits with NEED_GROW and resumes from its saved level 0; still exact
+    monkeypatch.setenv("PBH_SSSP_BASE1", "8192")
+    for g in (O.gen_random(20000, 400000, 1000, 4), O.gen_random(20000, 2000000, 1000, 6)):
+        check(pbh, O, g)
