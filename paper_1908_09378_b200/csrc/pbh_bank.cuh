@@ -1222,6 +1222,20 @@ __global__ void __launch_bounds__(32 * NW, 1)
       kb = tr.kinds[op + 2];
       eb = tr.offsets[op + 3];
     }
+    // a small next bulk op (<= 128 keys): its index entries into L2. The last
+    // warp loads the keys (already L2-resident) and prefetches their lines,
+    // overlapping this op's own gather latency (larger batches: the detour
+    // costs the warp more than the next op's gathers save)
+    if (tid >= B - 32 && op + 1 < op_end && (ka == 'U' || ka == 'B') && ea - hs_ <= 128) {
+      const u32 nn = (u32)(ea - hs_);
+      const u32 l = tid - (B - 32);
+      u32 kq[4];
+#pragma unroll
+      for (u32 q = 0; q < 4; ++q) kq[q] = l + 32 * q < nn ? tr.vals[hs_ + l + 32 * q] : 0xffffffffu;
+#pragma unroll
+      for (u32 q = 0; q < 4; ++q)
+        if (kq[q] < universe) asm volatile("prefetch.global.L2 [%0];" ::"l"(idx + kq[q]));
+    }
     if (kind == 'U' || kind == 'B') {
       // ------------------------------------------------ bulk_update / update
       const u32* vals = tr.vals + ob;
