@@ -334,7 +334,11 @@ cudaError_t launch_sssp_bank_nw(int nw, cudaStream_t st, u32 grid, pbh_heap_dev*
       return launch_sssp_bank<1, 32>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
     case 1: return launch_sssp_bank<1>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
     case 2: return launch_sssp_bank<2>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
-    case 4: return launch_sssp_bank<4>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
+    case 4:
+      // low-degree graphs (grids): one edge per thread per pass of 128
+      if (maxdeg <= 128)
+        return launch_sssp_bank<4, 128>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
+      return launch_sssp_bank<4>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
     default: return launch_sssp_bank<8>(st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, save, dag, maxdeg, d);
   }
 }
