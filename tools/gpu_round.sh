@@ -1,4 +1,2 @@
-for v in base p128; do echo "== $v"; cp variants/lib_$v.so paper_1908_09378_b200/libpbh_gpu.so
-timeout 300 python tools/probe.py band_small grid_small 2>&1 | grep -o '"name": "[^"]*"\|"ns_per_round": [0-9.]*' | paste - -
-done
-timeout 900 python -m pytest tests -m gpu -x -q -k "sssp or dijkstra or smoke" 2>&1 | tail -2
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -1
+timeout 1200 python tools/bench_suite.py c2 c3 > /dev/null 2> gpurun_out/suite_c2c3_final.jsonl; grep '^{' gpurun_out/suite_c2c3_final.jsonl | cut -c1-220
