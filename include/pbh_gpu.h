@@ -56,7 +56,9 @@ uint64_t pbh_launch_count(void);
  * (bucket_heap.cpp:11-15): d must be in [1, 2^40] else PBH_PRECONDITION.
  * key_universe: initial size of the per-key position index (keys are
  * u32 values); 0 picks a default. The index grows on demand for update
- * keys beyond it; deletes of keys beyond it are no-ops (absent values).
+ * keys beyond it; deletes of keys beyond it are no-ops (absent values) that
+ * are remembered, so a later insert of such a value is PBH_PRECONDITION
+ * like any re-insertion. key_universe > 2^32 -> PBH_PRECONDITION.
  * debug_checks mirrors EngineConfig::debug_assertions with workers == 1
  * (trace_checks, engine.cpp:23-24): priority increases are rejected. */
 pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int debug_checks,
@@ -69,7 +71,8 @@ pbh_status pbh_heap_destroy(pbh_heap* h);
  * value -> PBH_PRECONDITION (bucket_heap.cpp:55-58). */
 pbh_status pbh_heap_update(pbh_heap* h, uint32_t value, uint64_t priority);
 /* Engine::bulk_update(span) (engine.cpp:95-98; bucket_heap.cpp:127-146):
- * 1 <= n <= d, values strictly increasing, else PBH_PRECONDITION. */
+ * 1 <= n <= d, values strictly increasing, else PBH_PRECONDITION. Batches
+ * above 2^26 elements (the device batch buffers) are PBH_PRECONDITION too. */
 pbh_status pbh_heap_bulk_update(pbh_heap* h, const uint32_t* values, const uint64_t* priorities,
                                 uint64_t n);
 /* Engine::extract_min() (engine.cpp:100-104): PBH_EMPTY when no live value. */
@@ -195,6 +198,43 @@ pbh_status pbh_bellman_ford(const pbh_csr* g, uint32_t source, int device, uint6
  * speed; no reference counterpart (the reference is host-only). */
 pbh_status pbh_host_register(void* ptr, uint64_t bytes);
 pbh_status pbh_host_unregister(void* ptr);
+
+/* ---- CSR input contract (graphs.hpp:11-23) -------------------------------
+ * validate_graph (graphs.hpp:23, graphs.cpp:55-72) as one device pass over
+ * host or device arrays: PBH_INVARIANT with the reference's message for the
+ * violation its sequential loop would report first ("graph: inconsistent
+ * array sizes", "graph: offsets not monotone", "graph: target out of range",
+ * "graph: self-loop", "graph: row not sorted or parallel edge",
+ * "graph: zero weight"). The SSSP entry points (pbh_sssp*, pbh_sssp_ctx_create,
+ * pbh_sssp_ctx_load_graph, pbh_bellman_ford) run the same pass and return
+ * PBH_PRECONDITION for the violations that would make a kernel read out of
+ * bounds (sizes, offsets, targets >= V). */
+pbh_status pbh_validate_graph(const pbh_csr* g, int device);
+/* CsrGraph::max_out_degree() (graphs.hpp:18, graphs.cpp:47-53): on the host
+ * for host offsets, on `device` for device arrays. */
+pbh_status pbh_csr_max_out_degree(const pbh_csr* g, int device, uint32_t* out);
+
+/* ---- multi-source gather (BASELINE C5) --------------------
+ * Copy the dist / parent rows of source slots [first_slot, first_slot +
+ * n_slots) of the last pbh_sssp_ctx_run into dist_dst (n_slots x V u64) /
+ * parent_dst (n_slots x V u32), either nullable. The destination may be host
+ * memory, this device, a peer device (NVLink peer copy) or a buffer of
+ * another process mapped with pbh_ipc_open: one process per GPU gathers into
+ * GPU 0 without a collective. Blocking. */
+pbh_status pbh_sssp_ctx_gather(pbh_sssp_ctx* c, uint64_t first_slot, uint64_t n_slots,
+                               uint64_t* dist_dst, uint32_t* parent_dst);
+
+/* Device buffers shareable across processes (CUDA IPC): pbh_device_alloc on
+ * the gathering GPU, pbh_ipc_export its 64-byte handle, pbh_ipc_open it in
+ * each peer process (peer access enabled lazily), pbh_ipc_close when done.
+ * pbh_copy is a blocking copy between any two of host / device / peer /
+ * IPC-mapped memory. No reference counterpart (the reference is host-only). */
+pbh_status pbh_device_alloc(int device, uint64_t bytes, void** ptr);
+pbh_status pbh_device_free(int device, void* ptr);
+pbh_status pbh_ipc_export(void* dev_ptr, uint8_t handle[64]);
+pbh_status pbh_ipc_open(const uint8_t handle[64], int device, void** ptr);
+pbh_status pbh_ipc_close(int device, void* ptr);
+pbh_status pbh_copy(void* dst, const void* src, uint64_t bytes);
 
 /* distance_checksum (sssp.cpp:174-183): FNV-1a over the distance bytes. */
 uint64_t pbh_distance_checksum(const uint64_t* dist, uint64_t n);

@@ -101,6 +101,8 @@ def lib():
                                    U64P, U32P, U64P, U64P, U64P]
         L.orc_checksum.restype = C.c_uint64
         L.orc_checksum.argtypes = [U64P, C.c_uint64]
+        L.orc_fnv1a.restype = C.c_uint64
+        L.orc_fnv1a.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
         _lib = L
     return _lib
 
@@ -203,6 +205,27 @@ def checksum(dist):
     return int(lib().orc_checksum(_p(dist, U64P), len(dist)))
 
 
+FNV_BASIS = 0xcbf29ce484222325
+
+
+def fnv1a(*arrays, h=FNV_BASIS):
+    """FNV-1a (sssp.cpp:174-183's hash) over the raw little-endian bytes of
+    the arrays in order. fnv1a(settled_order) is the settle-order checksum of
+    the full-size goldens; fnv1a(vals, prios) the extraction-sequence one."""
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h = int(lib().orc_fnv1a(C.c_void_p(a.ctypes.data), a.nbytes, h))
+    return h
+
+
+def settle_order_from_dist(dist):
+    """The reference's settle order recomputed from dist: reached vertices by
+    (dist, vid) (SURVEY.md §8a semantic facts; test_sssp.cpp:92-100)."""
+    dist = np.asarray(dist, np.uint64)
+    reached = np.nonzero(dist != np.uint64(2 ** 64 - 1))[0].astype(np.uint32)
+    return reached[np.lexsort((reached, dist[reached]))]
+
+
 # --------------------------------------------------------------------------
 # The reference itself (oracle/_ref), available where it was built
 # --------------------------------------------------------------------------
@@ -245,6 +268,8 @@ def ref():
         L.ref_sssp.argtypes = [V, C.c_int, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int, C.c_int,
                                U64P, U32P, U64P, U64P, U64P]
         L.ref_sssp_multi.argtypes = [V, C.c_int, U32P, C.c_uint64, C.c_uint64, U64P]
+        L.ref_sssp_batch.argtypes = [V, C.c_int, U32P, C.c_uint64, C.c_uint64, C.c_uint64, U64P,
+                                     U64P, U64P, U64P, U64P, U64P, C.POINTER(C.c_double)]
         L.ref_bulk_sweep.argtypes = [C.c_uint64, C.c_uint64, U32P, U64P, C.c_uint64, U32P, U64P,
                                      C.POINTER(C.c_double)]
         L.ref_distance_checksum.restype = C.c_uint64
@@ -362,6 +387,44 @@ def ref_sssp_multi(g: Graph, sources, algo="par", threads=None):
     if st:
         raise RefError(st, L.ref_last_error().decode())
     return dist.reshape(len(src), g.V)
+
+
+class RefGraph:
+    """A CSR imported into the reference's CsrGraph ONCE (graph load is not
+    part of any timed CPU solve)."""
+
+    def __init__(self, g: Graph):
+        self.V, self.E = g.V, g.E
+        self._h = _ref_graph_handle(g)
+
+    def sssp_batch(self, sources, algo="par", threads=1, d=0, want_dist=False):
+        """ref_sssp_batch: independent sources on `threads` host threads.
+        Returns dict of per-source arrays (dist_ck, settled_ck, n_settled,
+        rounds, ops[, dist]) and the solve-only wall seconds."""
+        L = ref()
+        src = np.ascontiguousarray(sources, dtype=np.uint32)
+        n = len(src)
+        out = {k: np.zeros(n, np.uint64) for k in ("dist_ck", "settled_ck", "n_settled", "rounds", "ops")}
+        dist = np.zeros(n * self.V, np.uint64) if want_dist else None
+        secs = C.c_double()
+        st = L.ref_sssp_batch(self._h, {"par": 0, "ref": 1}[algo], _p(src, U32P), n, threads, d,
+                              _p(out["dist_ck"], U64P), _p(out["settled_ck"], U64P),
+                              _p(out["n_settled"], U64P), _p(out["rounds"], U64P),
+                              _p(out["ops"], U64P), _p(dist, U64P) if want_dist else None,
+                              C.byref(secs))
+        if st:
+            raise RefError(st, L.ref_last_error().decode())
+        if want_dist:
+            out["dist"] = dist.reshape(n, self.V)
+        out["seconds"] = secs.value
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            ref().ref_graph_free(self._h)
+            self._h = None
+
+    __del__ = close
 
 
 def ref_bulk_sweep(d, pre_v, pre_p, v, p):

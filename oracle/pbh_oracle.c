@@ -903,3 +903,15 @@ uint64_t orc_checksum(const uint64_t* dist, uint64_t n) {
     }
   return h;
 }
+
+/* FNV-1a (the hash of distance_checksum, sssp.cpp:174-183) over raw bytes,
+ * continued from h (start with PBH_FNV_BASIS). Used to fingerprint settle
+ * orders and extraction sequences for the full-size goldens. */
+uint64_t orc_fnv1a(const void* p, uint64_t n, uint64_t h) {
+  const unsigned char* b = (const unsigned char*)p;
+  for (uint64_t i = 0; i < n; ++i) {
+    h ^= b[i];
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}

@@ -82,6 +82,10 @@ int orc_dijkstra(uint32_t V, uint64_t E, const uint64_t* off, const uint32_t* tg
 /* distance_checksum (sssp.cpp:174-183): FNV-1a over the distance bytes. */
 uint64_t orc_checksum(const uint64_t* dist, uint64_t n);
 
+/* FNV-1a over n raw bytes continued from h; start from ORC_FNV_BASIS. */
+#define ORC_FNV_BASIS 0xcbf29ce484222325ULL
+uint64_t orc_fnv1a(const void* p, uint64_t n, uint64_t h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <atomic>
 #include <exception>
 #include <string>
 #include <thread>
@@ -266,6 +267,61 @@ int ref_sssp_multi(void* h, int algo, const std::uint32_t* sources, std::uint64_
     });
   }
   for (auto& th : pool) th.join();
+  for (int s : status)
+    if (s != kOk) return s;
+  return kOk;
+}
+
+std::uint64_t fnv1a(const void* p, std::size_t n, std::uint64_t h) {
+  const auto* b = static_cast<const unsigned char*>(p);
+  for (std::size_t i = 0; i < n; ++i) {
+    h ^= b[i];
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+/// Batch of independent sources on a graph imported ONCE (ref_graph_import /
+/// ref_graph_gen), for the goldens and the timed CPU baseline: graph import
+/// is outside *seconds (SPEC.md:602 excludes graph load). `threads` host
+/// threads pull sources from a shared counter. algo: 0 par_dijkstra
+/// (workers = 1, d = 0 -> max out-degree, sssp.cpp:21-69), 1 reference_dijkstra
+/// (sssp.cpp:71-97). Per source: distance_checksum (sssp.cpp:174-183), FNV-1a
+/// over the settled_order bytes (u32 LE), n_settled, rounds, metrics.ops.
+/// dist_out (nullable) receives n_sources x V distances.
+int ref_sssp_batch(void* h, int algo, const std::uint32_t* sources, std::uint64_t n_sources,
+                   std::uint64_t threads, std::uint64_t d, std::uint64_t* dist_ck,
+                   std::uint64_t* settled_ck, std::uint64_t* n_settled, std::uint64_t* rounds,
+                   std::uint64_t* ops, std::uint64_t* dist_out, double* seconds) {
+  const CsrGraph& g = static_cast<RefGraph*>(h)->g;
+  std::vector<int> status(n_sources, kOk);
+  std::atomic<std::uint64_t> next{0};
+  if (threads == 0) threads = 1;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (std::uint64_t t = 0; t < threads; ++t) {
+    pool.emplace_back([&] {
+      for (std::uint64_t s = next++; s < n_sources; s = next++) {
+        status[s] = guarded([&] {
+          SsspResult r = algo == 0 ? par_dijkstra(g, sources[s], EngineConfig{d, 1, false}, false)
+                                   : reference_dijkstra(g, sources[s]);
+          if (dist_ck) dist_ck[s] = distance_checksum(r.dist);
+          if (settled_ck)
+            settled_ck[s] = fnv1a(r.settled_order.data(), r.settled_order.size() * 4,
+                                  0xcbf29ce484222325ull);
+          if (n_settled) n_settled[s] = r.settled_order.size();
+          if (rounds) rounds[s] = r.rounds;
+          if (ops) ops[s] = r.metrics.ops;
+          if (dist_out)
+            std::memcpy(dist_out + s * g.vertex_count, r.dist.data(),
+                        r.dist.size() * sizeof(std::uint64_t));
+        });
+      }
+    });
+  }
+  for (auto& th : pool) th.join();
+  if (seconds)
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   for (int s : status)
     if (s != kOk) return s;
   return kOk;

@@ -8,6 +8,6 @@ from .errors import (DeviceError, EmptyHeapError, InvariantError, PreconditionEr
                      TraceError)
 from .heap import Element, Engine, EngineConfig, Metrics, RunResult  # noqa: F401
 from .sssp import (K_INF_DIST, CsrGraph, bellman_ford, SsspContext, SsspResult, distance_checksum,  # noqa: F401
-                   distances_to_csv, par_dijkstra, par_dijkstra_multi, par_dijkstra_multi_device,
-                   pin, threshold_sssp, unpin,
-                   validate_parent_tree)
+                   certify_distances, distances_to_csv, max_out_degree, par_dijkstra,
+                   par_dijkstra_multi, par_dijkstra_multi_device, pin, threshold_sssp, unpin,
+                   validate_graph, validate_parent_tree)

@@ -67,6 +67,15 @@ SIGNATURES = {
                                    C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                    C.POINTER(C.c_double)]),
     "pbh_host_unregister": (C.c_int, [C.c_void_p]),
+    "pbh_validate_graph": (C.c_int, [C.POINTER(Csr), C.c_int]),
+    "pbh_csr_max_out_degree": (C.c_int, [C.POINTER(Csr), C.c_int, U32P]),
+    "pbh_sssp_ctx_gather": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "pbh_device_alloc": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]),
+    "pbh_device_free": (C.c_int, [C.c_int, C.c_void_p]),
+    "pbh_ipc_export": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8)]),
+    "pbh_ipc_open": (C.c_int, [C.POINTER(C.c_uint8), C.c_int, C.POINTER(C.c_void_p)]),
+    "pbh_ipc_close": (C.c_int, [C.c_int, C.c_void_p]),
+    "pbh_copy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
 }
 
 _lib = None

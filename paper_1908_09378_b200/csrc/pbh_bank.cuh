@@ -1140,7 +1140,8 @@ __global__ void __launch_bounds__(32 * NW, 1)
   H.prof = prof;
   pbh_idx_entry* const idx = g->idx;
   const u64 universe = g->universe;
-  const u32 dmax = sm.d;
+  // batches beyond the large-batch buffers (2^26 entries) are rejected, not split
+  const u32 dmax = min(sm.d, kMaxBatch);
   const bool debug = sm.debug != 0;
   // restore the level-0 image
   {
@@ -1532,6 +1533,20 @@ __global__ void __launch_bounds__(32 * NW, 1)
           --live;
         }
         if (tid == 0) idx[k].state = PBH_ST_DEAD;  // deeper copies are now stale
+        Bk::sync();
+      } else {
+        // beyond the index: an absent value (no-op), remembered so that the
+        // index growth that later covers it marks it DEAD; a full list makes
+        // the host grow the index now
+        const u32 on = *(volatile u32*)&g->oor_n;
+        if (on >= g->oor_cap) {
+          hc.fail(PBH_ERR_KEY_RANGE, k);
+          break;
+        }
+        if (tid == 0) {
+          g->oor_del[on] = k;
+          *(volatile u32*)&g->oor_n = on + 1;
+        }
         Bk::sync();
       }
     } else if (kind == kOpDrain && allow_internal) {

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <map>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -19,6 +20,7 @@
 #include "pbh_bf.cuh"
 #include "pbh_multi.cuh"
 #include "pbh_gen_gpu.cuh"
+#include "pbh_csr.cuh"
 #include "../../include/pbh_gen.h"
 
 using namespace pbh_dev;
@@ -42,136 +44,23 @@ pbh_status set_err(pbh_status s, const std::string& msg) {
   } while (0)
 
 constexpr int VT = 4;
-constexpr u32 kSmemLimit = 227 * 1024;
+constexpr u32 kOorCap = 4096;  // remembered out-of-index deletes per heap
 
 u64 pow2_at_least(u64 x) {
   u64 p = 1;
   while (p < x) p <<= 1;
   return p;
 }
-u32 a16(u64 x) { return (u32)((x + 15) & ~u64(15)); }
 
-template <int NT>
-size_t heap_smem_bytes() {
-  return sizeof(HeapSmem<NT, VT>);
-}
+// Per-device launch attributes: the dynamic shared-memory opt-in is a
+// per-device property, and the cooperative grid size depends on the device.
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, int> g_grid_of;  // (kernel, device) -> grid
 
-size_t heap_smem_bytes_nt(int nt) {
-  switch (nt) {
-    case 32: return heap_smem_bytes<32>();
-    case 256: return heap_smem_bytes<256>();
-    default: return heap_smem_bytes<1024>();
-  }
-}
-
-size_t grid_smem_bytes_nt(int nt) {
-  switch (nt) {
-    case 32: return sizeof(GridSmem<32>);
-    case 256: return sizeof(GridSmem<256>);
-    default: return sizeof(GridSmem<1024>);
-  }
-}
-
-SmLayout make_layout(int nt, u32 cap0, u32 bc, u32 d, bool sssp) {
-  SmLayout L{};
-  u32 off = a16(heap_smem_bytes_nt(nt));
-  if (!sssp) {
-    L.off_grid = off;
-    off += a16(grid_smem_bytes_nt(nt));
-    L.grid_min = kGridMin;
-    if (const char* e = getenv("PBH_GRID_MIN")) L.grid_min = std::max(2, atoi(e));
-  }
-  const u32 base = off;
-  L.off_b0k0 = off; off += a16((u64)cap0 * 4);
-  L.off_b0k1 = off; off += a16((u64)cap0 * 4);
-  L.off_b0p0 = off; off += a16((u64)cap0 * 8);
-  L.off_b0p1 = off; off += a16((u64)cap0 * 8);
-  L.off_bk = off; off += a16((u64)bc * 4);
-  L.off_bp = off; off += a16((u64)bc * 8);
-  L.off_pk = off; off += a16((u64)bc * 4);
-  L.off_pp = off; off += a16((u64)bc * 8);
-  L.off_rm = off; off += a16(cap0);
-  if (sssp) {
-    const u64 cc = (u64)d + nt;
-    L.off_ck = off; off += a16(cc * 4);
-    L.off_cp = off; off += a16(cc * 8);
-    L.off_co = off; off += a16(cc * 8);
-    L.off_cs = off; off += a16(cc * 4);
-  }
-  if (off <= kSmemLimit) {
-    L.use_smem = 1;
-    L.total = off;
-  } else {
-    L.use_smem = 0;
-    L.total = base;
-  }
-  return L;
-}
-
-int pick_nt(u64 d) {
-  if (const char* e = getenv("PBH_NT")) return atoi(e);
-  // deep-level merges dominate small batches: a 256-thread CTA beats a warp
-  // even at d = 1 (C4 prefill at d = 32: 95 -> 28 us per op)
-  if (d <= 256) return 256;
-  return 1024;
-}
-
-u32 pick_cap0(u64 d) {
-  u64 c0min = 256;
-  if (const char* e = getenv("PBH_CAP0_MIN")) c0min = strtoull(e, nullptr, 10);
-  u64 c = std::max<u64>(2 * d, c0min);
-  c = std::min<u64>(c, 1ull << 22);
-  return (u32)c;
-}
-
-// ------------------------------------------------------------ kernel table
-// The trace interpreter: CTA 0 replays the ops; with gj, CTAs 1..G-1 are the
-// grid helpers of pbh_grid.cuh (cooperative launch = guaranteed co-residency,
-// one CTA per SM).
-template <int NT>
-cudaError_t launch_trace(const SmLayout& L, cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr,
-                         u64 b, u64 e, u32* ov, u64* op, pbh_kstatus* ks, u32 internal,
-                         GridJob* gj) {
-  auto fn = k_trace<NT, VT>;
-  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
-  if (err != cudaSuccess) return err;
-  int G = 1;
-  if (gj) {
-    static int grid_cache[3] = {0, 0, 0};
-    int& gc = grid_cache[NT == 32 ? 0 : NT == 256 ? 1 : 2];
-    if (gc == 0) {
-      int dev = 0, sms = 0, per_sm = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, L.total);
-      gc = std::max(1, sms * std::min(per_sm, 1));
-      if (const char* s = getenv("PBH_GRID")) gc = std::max(1, std::min(gc, atoi(s)));
-    }
-    G = gc;
-  }
-  if (G > 1) {
-    err = cudaMemsetAsync(gj, 0, sizeof(GridJob), st);
-    if (err != cudaSuccess) return err;
-    SmLayout Lc = L;
-    u32 internal_c = internal;
-    void* args[] = {&g, &tr, &b, &e, &ov, &op, &ks, &Lc, &internal_c, &gj};
-    err = cudaLaunchCooperativeKernel((const void*)fn, dim3(G), dim3(NT), args, L.total, st);
-  } else {
-    fn<<<1, NT, L.total, st>>>(g, tr, b, e, ov, op, ks, L, internal, gj);
-    err = cudaGetLastError();
-  }
-  g_launches++;
-  return err;
-}
-
-cudaError_t launch_trace_nt(int nt, const SmLayout& L, cudaStream_t st, pbh_heap_dev* g,
-                            pbh_trace_dev tr, u64 b, u64 e, u32* ov, u64* op, pbh_kstatus* ks,
-                            u32 internal, GridJob* gj) {
-  switch (nt) {
-    case 32: return launch_trace<32>(L, st, g, tr, b, e, ov, op, ks, internal, gj);
-    case 256: return launch_trace<256>(L, st, g, tr, b, e, ov, op, ks, internal, gj);
-    default: return launch_trace<1024>(L, st, g, tr, b, e, ov, op, ks, internal, gj);
-  }
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
 }
 
 // Banked op-trace interpreter (pbh_bank.cuh): 4 warps, level 0 = 1024 slots.
@@ -186,18 +75,21 @@ cudaError_t launch_trace_bank(cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr
                               BatchJob* bj) {
   auto fn = k_trace_bank<kTraceNW, kTraceKI, VT>;
   const int smem = (int)sizeof(TraceSmem);
-  static int G = 0;
-  if (G == 0) {
-    cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (err != cudaSuccess) return err;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kTraceNW, smem);
-    G = std::max(1, sms * std::min(per_sm, 1));
-    if (const char* s = getenv("PBH_GRID")) G = std::max(1, std::min(G, atoi(s)));
+  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (err != cudaSuccess) return err;
+  int G = 0;
+  {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int& gc = g_grid_of[{(const void*)fn, dev}];
+    if (gc == 0) {
+      int sms = 0, per_sm = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kTraceNW, smem);
+      gc = std::max(1, sms * std::min(per_sm, 1));
+    }
+    G = gc;
   }
-  cudaError_t err;
   if (gj && G > 1) {
     err = cudaMemsetAsync(gj, 0, sizeof(GridJob), st);
     if (err != cudaSuccess) return err;
@@ -211,30 +103,6 @@ cudaError_t launch_trace_bank(cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr
   g_launches++;
   return err;
 }
-
-template <int NT>
-cudaError_t launch_sssp(const SmLayout& L, cudaStream_t st, u32 grid, pbh_heap_dev* heaps,
-                        const u64* off, const u32* tgt, const u32* w, u32 V, const u32* src,
-                        u64* dist, u32* settled, SsspState* sst, u32 dag, u32 maxdeg) {
-  auto fn = k_sssp<NT, VT>;
-  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
-  if (err != cudaSuccess) return err;
-  fn<<<grid, NT, L.total, st>>>(heaps, off, tgt, w, V, src, dist, settled, sst, dag, maxdeg, L);
-  g_launches++;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_sssp_nt(int nt, const SmLayout& L, cudaStream_t st, u32 grid,
-                           pbh_heap_dev* heaps, const u64* off, const u32* tgt, const u32* w, u32 V,
-                           const u32* src, u64* dist, u32* settled, SsspState* sst, u32 dag,
-                           u32 maxdeg) {
-  switch (nt) {
-    case 32: return launch_sssp<32>(L, st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, dag, maxdeg);
-    case 256: return launch_sssp<256>(L, st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, dag, maxdeg);
-    default: return launch_sssp<1024>(L, st, grid, heaps, off, tgt, w, V, src, dist, settled, sst, dag, maxdeg);
-  }
-}
-
 
 // Banked level-0 SSSP engine variants: NW warps per source, KI slots per
 // thread, level 0 = 32*NW*KI = 1024 slots.
@@ -266,12 +134,9 @@ cudaError_t launch_sssp_bank(cudaStream_t st, u32 grid, pbh_heap_dev* heaps, con
   constexpr int KI = BankCfg<NW>::KI;
   auto fn = k_sssp_bank<NW, KI, VT, PASS>;
   const int smem = (int)sizeof(BankSmem<NW, KI, VT>);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  // per launch: the attribute is per device, and the call is cheap
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
   static unsigned long long* prof = nullptr;
   if (getenv("PBH_PHASES") && !prof && cudaMalloc(&prof, 64 * 8) == cudaSuccess) cudaMemset(prof, 0, 64 * 8);
   fn<<<grid, 32 * NW, smem, st>>>(heaps, off, tgt, w, V, src, dist, settled, sst,
@@ -313,12 +178,8 @@ cudaError_t launch_sssp_multi(cudaStream_t st, u32 grid, pbh_heap_dev* heaps, co
                               u32 maxdeg, u32 d) {
   auto fn = k_sssp_multi<4, 8, VT>;
   const int smem = (int)sizeof(MultiSmem<4, 8, VT>);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
   fn<<<grid, 128, smem, st>>>(heaps, off, tgt, w, mwo, mwi, V, src, dist, settled, sst,
                               reinterpret_cast<MultiImage*>(save), maxdeg, d);
   g_launches++;
@@ -350,18 +211,12 @@ __global__ void k_finalize_parent(const pbh_idx_entry* idx, u32 V, u32* parent) 
   }
 }
 
-__global__ void k_max_degree(const u64* off, u32 V, unsigned long long* out) {
-  u64 best = 0;
-  for (u64 v = blockIdx.x * (u64)blockDim.x + threadIdx.x; v < V; v += (u64)gridDim.x * blockDim.x)
-    best = max(best, off[v + 1] - off[v]);
-  atomicMax(out, (unsigned long long)best);
-}
 
 const char* detail_message(u32 detail) {
   switch (detail) {
     case PBH_ERR_EMPTY_HEAP: return "extract_min: heap is empty";
     case PBH_ERR_EMPTY_BATCH: return "bulk_update: empty batch";
-    case PBH_ERR_BATCH_TOO_BIG: return "bulk_update: batch larger than d";
+    case PBH_ERR_BATCH_TOO_BIG: return "bulk_update: batch larger than d (or the 2^26-element batch limit)";
     case PBH_ERR_UNSORTED: return "bulk_update: batch must be value-sorted with unique values";
     case PBH_ERR_REINSERT: return "update: value was already extracted or deleted; re-insertion is unsupported";
     case PBH_ERR_INCREASE: return "update: priority increase";
@@ -473,6 +328,9 @@ pbh_status init_heap(DevHeap& H, u64 d, u32 cap0, u32 bc, u32 nt, u64 universe, 
   if ((st = alloc_scratch(H, bc, nt, strm))) return st;
   H.hd.universe = universe;
   if ((st = H.alloc((void**)&H.hd.idx, universe * sizeof(pbh_idx_entry)))) return st;
+  H.hd.oor_cap = kOorCap;
+  H.hd.oor_n = 0;
+  if ((st = H.alloc((void**)&H.hd.oor_del, kOorCap * sizeof(u32)))) return st;
   if (dev_slot) {
     H.dev = dev_slot;
   } else {
@@ -483,6 +341,11 @@ pbh_status init_heap(DevHeap& H, u64 d, u32 cap0, u32 bc, u32 nt, u64 universe, 
   CK(cudaMemcpyAsync(H.dev, &H.hd, sizeof(pbh_heap_dev), cudaMemcpyHostToDevice, strm));
   if (strm == 0) CK(cudaStreamSynchronize(0));
   return PBH_OK;
+}
+
+__global__ void k_mark_dead(pbh_idx_entry* idx, u64 universe, const u32* keys, u32 n) {
+  for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (keys[i] < universe) idx[keys[i]].state = PBH_ST_DEAD;
 }
 
 // Pull the mutable header back, add one level, push it again.
@@ -516,6 +379,18 @@ pbh_status grow_universe(DevHeap& H, cudaStream_t s, u64 want) {
   }
   H.hd.idx = ni;
   H.hd.universe = nu;
+  // deletes recorded beyond the old index: the values they cover are DEAD
+  if (H.hd.oor_n) {
+    k_mark_dead<<<1, 256, 0, s>>>(ni, nu, H.hd.oor_del, H.hd.oor_n);
+    g_launches++;
+    std::vector<u32> keep(H.hd.oor_n);
+    CK(cudaMemcpyAsync(keep.data(), H.hd.oor_del, keep.size() * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    keep.erase(std::remove_if(keep.begin(), keep.end(), [&](u32 k) { return k < nu; }), keep.end());
+    if (!keep.empty())
+      CK(cudaMemcpyAsync(H.hd.oor_del, keep.data(), keep.size() * 4, cudaMemcpyHostToDevice, s));
+    H.hd.oor_n = (u32)keep.size();
+  }
   CK(cudaMemcpyAsync(H.dev, &H.hd, sizeof(pbh_heap_dev), cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));
   return PBH_OK;
@@ -532,11 +407,9 @@ struct pbh_heap {
   u64 d = 1;
   int nt = 32;
   DevHeap H;
-  SmLayout layout{};
   pbh_kstatus* d_ks = nullptr;
   pbh_kstatus* h_ks = nullptr;  // pinned
   GridJob* d_job = nullptr;     // grid-helper job word (null: single-CTA engine)
-  bool bank = true;             // banked level-0 interpreter (false: sorted-B_0 CTA engine)
   TraceImage* d_save = nullptr; // its level-0 image between launches
   u32 grid_min = kGridMin;
   unsigned long long* d_prof = nullptr;  // PBH_PROF: leader cycle breakdown
@@ -582,25 +455,6 @@ pbh_status ensure_staging(pbh_heap* h, u64 n_ops, u64 n_el, u64 n_out) {
   return PBH_OK;
 }
 
-// Make sure the batch scratch can hold batches of up to n elements.
-pbh_status ensure_batch(pbh_heap* h, u64 n) {
-  if (h->bank || n <= h->H.bc) return PBH_OK;  // the banked engine needs no batch scratch
-  u32 bc = (u32)pow2_at_least(n);
-  DevHeap& H = h->H;
-  CK(cudaMemcpyAsync(&H.hd, H.dev, sizeof(pbh_heap_dev), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
-  pbh_status st;
-  if ((st = H.alloc((void**)&H.hd.g_bk, (u64)bc * 4))) return st;
-  if ((st = H.alloc((void**)&H.hd.g_bp, (u64)bc * 8))) return st;
-  if ((st = H.alloc((void**)&H.hd.g_pk, (u64)bc * 4))) return st;
-  if ((st = H.alloc((void**)&H.hd.g_pp, (u64)bc * 8))) return st;
-  H.bc = bc;
-  CK(cudaMemcpyAsync(H.dev, &H.hd, sizeof(pbh_heap_dev), cudaMemcpyHostToDevice, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
-  h->layout = make_layout(h->nt, H.hd.cap0, H.bc, H.hd.d, false);
-  return PBH_OK;
-}
-
 // Run ops [0, n_ops) of a device trace with the NEED_GROW / KEY_RANGE resume
 // loop. host_vals: host copy of the values (for universe growth) or null.
 pbh_status exec_trace(pbh_heap* h, u64 n_ops, pbh_trace_dev tr, u32* d_ov, u64* d_op,
@@ -612,13 +466,8 @@ pbh_status exec_trace(pbh_heap* h, u64 n_ops, pbh_trace_dev tr, u32* d_ov, u64* 
   for (int guard = 0; guard < 4096; ++guard) {
     if (begin >= n_ops) break;
     CK(cudaEventRecord(h->ev0, h->stream));
-    if (h->bank) {
-      CK(launch_trace_bank(h->stream, h->H.dev, tr, begin, n_ops, d_ov, d_op, h->d_ks, h->d_save,
-                           internal, h->d_job, h->grid_min, h->d_prof, h->d_batch));
-    } else {
-      CK(launch_trace_nt(h->nt, h->layout, h->stream, h->H.dev, tr, begin, n_ops, d_ov, d_op,
-                         h->d_ks, internal, h->d_job));
-    }
+    CK(launch_trace_bank(h->stream, h->H.dev, tr, begin, n_ops, d_ov, d_op, h->d_ks, h->d_save,
+                         internal, h->d_job, h->grid_min, h->d_prof, h->d_batch));
     CK(cudaEventRecord(h->ev1, h->stream));
     CK(cudaMemcpyAsync(h->h_ks, h->d_ks, sizeof(pbh_kstatus), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -684,8 +533,8 @@ pbh_status exec_host(pbh_heap* h, u64 n_ops, const u8* kinds, const u64* off, co
     n_x += kinds[i] == 'E' || kinds[i] == 'F';
     if (kinds[i] == 'B') max_batch = std::max<u64>(max_batch, off[i + 1] - off[i]);
   }
+  (void)max_batch;
   pbh_status st;
-  if ((st = ensure_batch(h, std::min<u64>(max_batch, h->d)))) return st;
   if ((st = ensure_staging(h, n_ops, n_el, n_x))) return st;
   CK(cudaMemcpyAsync(h->d_kinds, kinds, n_ops, cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemcpyAsync(h->d_off, off, (n_ops + 1) * 8, cudaMemcpyHostToDevice, h->stream));
@@ -734,11 +583,10 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
   pbh_heap* h = new pbh_heap();
   h->device = device;
   h->d = d;
-  h->nt = pick_nt(d);
-  if (const char* e = getenv("PBH_TRACE_ENGINE")) h->bank = std::string(e) != "cta";
-  if (h->bank) h->nt = 32 * kTraceNW;
+  h->nt = 32 * kTraceNW;
   if (key_universe == 0) key_universe = 1 << 16;
-  const u32 cap0 = h->bank ? (u32)(32 * kTraceNW * kTraceKI / 2) : pick_cap0(d);
+  if (key_universe > (1ull << 32)) return set_err(PBH_PRECONDITION, "key_universe exceeds 2^32");
+  const u32 cap0 = (u32)(32 * kTraceNW * kTraceKI / 2);
   const u32 bc = (u32)pow2_at_least(std::max<u64>(std::min<u64>(d, 4096), 2));
   auto fail = [&](pbh_status s) {
     h->H.free_all();
@@ -750,15 +598,12 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
   // the banked engine pre-allocates levels for the key universe (each
   // NEED_GROW is a kernel exit + relaunch)
   u32 nlev = 2;
-  if (h->bank) {
-    // level 1 holds four push-buffer flushes, or four whole large batches
-    h->H.bank = true;
-    h->H.base1 = std::max<u64>(4ull * kBankQ, 4 * std::min<u64>(d, 1ull << 26));
-    while (nlev < 12 && (h->H.base1 << (2 * (nlev - 2))) < 2 * key_universe + 4 * kBankQ) ++nlev;
-  }
+  // level 1 holds four push-buffer flushes, or four whole large batches
+  h->H.bank = true;
+  h->H.base1 = std::max<u64>(4ull * kBankQ, 4 * std::min<u64>(d, kMaxBatch));
+  while (nlev < 12 && (h->H.base1 << (2 * (nlev - 2))) < 2 * key_universe + 4 * kBankQ) ++nlev;
   pbh_status st = init_heap(h->H, d, cap0, bc, h->nt, key_universe, debug_checks, nlev, nullptr);
   if (st) return fail(st);
-  h->layout = make_layout(h->nt, cap0, h->H.bc, h->H.hd.d, false);
   if (cudaMalloc(&h->d_ks, sizeof(pbh_kstatus)) != cudaSuccess ||
       cudaMallocHost(&h->h_ks, sizeof(pbh_kstatus)) != cudaSuccess)
     return fail(set_err(PBH_OOM, "status block allocation failed"));
@@ -766,7 +611,7 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
   const char* ge = getenv("PBH_GRID");
   if (!(ge && atoi(ge) <= 1) && cudaMalloc(&h->d_job, sizeof(GridJob)) != cudaSuccess)
     return fail(set_err(PBH_OOM, "grid job allocation failed"));
-  if (h->bank) {
+  {
     if (cudaMalloc(&h->d_save, sizeof(TraceImage)) != cudaSuccess)
       return fail(set_err(PBH_OOM, "level-0 image allocation failed"));
     TraceImage* img = new TraceImage();
@@ -777,9 +622,9 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
     if (e != cudaSuccess) return fail(set_err(PBH_CUDA, "level-0 image init failed"));
   }
   if (const char* e = getenv("PBH_GRID_MIN")) h->grid_min = std::max(2, atoi(e));
-  if (h->bank && h->d_job && d >= kBigBatch) {
+  if (h->d_job && d >= kBigBatch) {
     // large batches: job block + staging / sort ping-pong / leader list
-    const u64 cap = std::min<u64>(d, 1ull << 26);
+    const u64 cap = std::min<u64>(d, kMaxBatch);
     BatchJob hb{};
     void* mem[6] = {};
     const size_t sz[6] = {sizeof(BatchJob), cap * 4, cap * 8, cap * 4, cap * 8, cap * 4};
@@ -847,6 +692,8 @@ pbh_status pbh_heap_bulk_update(pbh_heap* h, const uint32_t* values, const uint6
   if (!h) return set_err(PBH_PRECONDITION, "null heap");
   if (n == 0) return set_err(PBH_PRECONDITION, "bulk_update: empty batch");
   if (n > h->d) return set_err(PBH_PRECONDITION, "bulk_update: batch larger than d");
+  if (n > kMaxBatch)
+    return set_err(PBH_PRECONDITION, "bulk_update: batch larger than the 2^26-element batch limit");
   for (u64 i = 1; i < n; ++i)
     if (values[i - 1] >= values[i])
       return set_err(PBH_PRECONDITION, "bulk_update: batch must be value-sorted with unique values");
@@ -945,7 +792,7 @@ pbh_status pbh_heap_check_invariants(pbh_heap* h, uint64_t* n_violations) {
   auto valid0 = [&](u32 k, u64 p) {
     return k < hd.universe && PBH_ST(idx[k].state) == PBH_ST_LIVE && idx[k].prio == p;
   };
-  if (h->bank) {
+  {
     // banked level 0 (pbh_bank.cuh): every occupied slot holds a valid entry
     // whose index records that slot, all admitted by splitter_0; the push
     // buffer holds entries beyond it
@@ -1061,6 +908,11 @@ pbh_status pbh_heap_run_trace(pbh_heap* h, uint64_t n_ops, const uint8_t* kinds,
     const u8 k = kinds[i];
     const bool ok = (k == 'U' && len == 1) || (k == 'B') || (k == 'E' && len == 0) ||
                     (k == 'D' && len == 1);
+    if (ok && k == 'B' && len > kMaxBatch) {  // larger than the device batch buffers
+      if (failed_op) *failed_op = i;
+      return set_err(PBH_TRACE, "op " + std::to_string(i) +
+                                    ": bulk_update: batch larger than the 2^26-element batch limit");
+    }
     if (!ok || offsets[i + 1] < offsets[i]) {
       if (failed_op) *failed_op = i;
       return set_err(PBH_TRACE, "op " + std::to_string(i) + ": malformed op");
@@ -1090,10 +942,7 @@ pbh_status pbh_heap_run_trace_device(pbh_heap* h, uint64_t n_ops, const uint8_t*
   cudaSetDevice(h->device);
   if (failed_op) *failed_op = ~0ull;
   pbh_trace_dev tr{d_kinds, d_offsets, d_values, d_priorities};
-  // batch scratch must cover the largest batch: bounded by d
-  pbh_status st = ensure_batch(h, std::min<u64>(h->d, 1ull << 26));
-  if (st) return st;
-  st = exec_trace(h, n_ops, tr, d_out_values, d_out_priorities, n_out, failed_op, 0, wall_ms,
+  pbh_status st = exec_trace(h, n_ops, tr, d_out_values, d_out_priorities, n_out, failed_op, 0, wall_ms,
                   nullptr, nullptr, nullptr);
   if (st == PBH_EMPTY || st == PBH_PRECONDITION) return set_err(PBH_TRACE, g_last_error);
   if (st) return st;
@@ -1104,6 +953,63 @@ pbh_status pbh_heap_run_trace_device(pbh_heap* h, uint64_t n_ops, const uint8_t*
   if (wall_ms) *wall_ms += dms;
   return st;
 }
+
+// =========================================================================
+// CSR input contract (graphs.cpp:47-72)
+// =========================================================================
+namespace {
+
+bool device_accessible(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Run k_csr_check over device arrays; blocking.
+pbh_status csr_check(cudaStream_t s, CsrCheck* d_chk, const u64* off, const u32* tgt, const u32* w,
+                     u32 V, u64 E, CsrCheck* out) {
+  CsrCheck init{};
+  init.first = ~0ull;
+  CK(cudaMemcpyAsync(d_chk, &init, sizeof init, cudaMemcpyHostToDevice, s));
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const u64 warps = std::max<u64>(1, std::min<u64>((u64)V, (u64)sms * 64));
+  k_csr_check<<<(u32)((warps * 32 + 255) / 256), 256, 0, s>>>(off, tgt, w, V, E, d_chk);
+  g_launches++;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, d_chk, sizeof *out, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return PBH_OK;
+}
+
+// validate_graph's messages (graphs.cpp:56-71) for the first violation.
+std::string csr_message(const CsrCheck& k) {
+  if (k.sizes_bad) return "graph: inconsistent array sizes";
+  switch ((u32)(k.first & 7)) {
+    case kCsrMonotone: return "graph: offsets not monotone";
+    case kCsrRange: return "graph: target out of range";
+    case kCsrSelfLoop: return "graph: self-loop";
+    case kCsrUnsorted: return "graph: row not sorted or parallel edge";
+    default: return "graph: zero weight";
+  }
+}
+
+// What the SSSP kernels cannot survive (out-of-bounds reads): bad sizes,
+// non-monotone offsets, targets >= V. Self-loops, unsorted rows and zero
+// weights are legal inputs to par_dijkstra (it does not call validate_graph).
+pbh_status csr_precondition(const CsrCheck& k, const char* who) {
+  const u32 code = (u32)(k.first & 7);
+  if (k.sizes_bad || (k.first != ~0ull && (code == kCsrMonotone || code == kCsrRange)))
+    return set_err(PBH_PRECONDITION, std::string(who) + ": " + csr_message(k) + " (vertex " +
+                                         std::to_string(k.first >> 32) + ")");
+  return PBH_OK;
+}
+
+}  // namespace
 
 // =========================================================================
 // SSSP
@@ -1121,15 +1027,13 @@ struct pbh_sssp_ctx {
   int nt = 32;
   u32 cap0 = 0;
   u64 max_sources = 0;
-  SmLayout layout{};
-  bool fast = true;   // banked engine (false: the sorted-B_0 CTA engine, PBH_SSSP_ENGINE=cta)
-  bool lane = true;   // banked level 0 (default)
-  int bank_nw = 1;    // warps per source of the banked engine
+  bool graph_ok = false;  // the resident CSR passed the device check
+  int bank_nw = 4;    // warps per source of the banked engine
   void* d_save = nullptr;
   bool multi = false;  // threshold multi-extraction (pbh_sssp_ctx_set_mode)
   u32* d_mwo = nullptr;
   u32* d_mwi = nullptr;
-  unsigned long long* d_md = nullptr;  // max out-degree scratch
+  CsrCheck* d_chk = nullptr;  // CSR check / max out-degree scratch
   std::vector<DevHeap> heaps;
   pbh_heap_dev* d_heaps = nullptr;
   SsspState* d_sst = nullptr;
@@ -1191,41 +1095,33 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
       (c->E && cudaMemcpyAsync(c->d_tgt, g->targets, c->E * 4, cudaMemcpyDefault, c->stream)) ||
       (c->E && cudaMemcpyAsync(c->d_w, g->weights, c->E * 4, cudaMemcpyDefault, c->stream)))
     return fail(set_err(PBH_CUDA, "CSR upload failed"));
-  // max out-degree on the device (graphs.cpp:47-53)
-  unsigned long long*& d_md = c->d_md;
-  if ((st = ctx_alloc(c, (void**)&d_md, 8))) return fail(st);
-  cudaMemsetAsync(d_md, 0, 8, c->stream);
-  k_max_degree<<<std::max<u32>(1, std::min<u32>(1184, (c->V + 255) / 256)), 256, 0, c->stream>>>(
-      c->d_off, c->V, d_md);
-  g_launches++;
-  unsigned long long md = 0;
-  cudaMemcpyAsync(&md, d_md, 8, cudaMemcpyDeviceToHost, c->stream);
-  if (cudaStreamSynchronize(c->stream) != cudaSuccess)
-    return fail(set_err(PBH_CUDA, "max-degree kernel failed"));
+  // the input contract and max out-degree on the device, one HBM pass
+  // (graphs.cpp:47-72): malformed offsets or targets >= V would make the
+  // kernels read out of bounds, so they fail here with PBH_PRECONDITION
+  if ((st = ctx_alloc(c, (void**)&c->d_chk, sizeof(CsrCheck)))) return fail(st);
+  CsrCheck chk{};
+  if ((st = csr_check(c->stream, c->d_chk, c->d_off, c->d_tgt, c->d_w, c->V, c->E, &chk)))
+    return fail(st);
+  if ((st = csr_precondition(chk, "par_dijkstra"))) return fail(st);
+  c->graph_ok = true;
+  const u64 md = chk.max_deg;
   c->max_deg = (u32)md;
   c->d = d ? d : std::max<u64>(1, md);  // sssp.cpp:24-26
   c->d = std::min<u64>(c->d, std::max<u64>(1, md ? md : 1));  // batches never exceed a row
-  c->nt = pick_nt(std::max<u64>(c->d, std::min<u64>(md, 1024)));
-  c->cap0 = pick_cap0(c->d);
-  if (const char* e = getenv("PBH_SSSP_ENGINE")) c->fast = c->lane = std::string(e) != "cta";
-  if (c->lane) {
+  c->bank_nw = 4;
+  if (const char* e = getenv("PBH_SSSP_NW")) c->bank_nw = atoi(e);
+  if (c->bank_nw != 0 && c->bank_nw != 1 && c->bank_nw != 2 && c->bank_nw != 4 && c->bank_nw != 8)
     c->bank_nw = 4;
-    if (const char* e = getenv("PBH_SSSP_NW")) c->bank_nw = atoi(e);
-    if (c->bank_nw != 0 && c->bank_nw != 1 && c->bank_nw != 2 && c->bank_nw != 4 && c->bank_nw != 8)
-      c->bank_nw = 4;
-    c->cap0 = kBankC0 / 2;
-    c->nt = 32 * std::max(c->bank_nw, 1);
-  }
+  c->cap0 = kBankC0 / 2;
+  c->nt = 32 * std::max(c->bank_nw, 1);
   const u32 bc = (u32)pow2_at_least(std::max<u64>(c->d, 2));
-  c->layout = make_layout(c->nt, c->cap0, bc, (u32)c->d, true);
   if ((st = ctx_alloc(c, (void**)&c->d_heaps, max_sources * sizeof(pbh_heap_dev)))) return fail(st);
   if ((st = ctx_alloc(c, (void**)&c->d_sst, max_sources * sizeof(SsspState)))) return fail(st);
   if ((st = ctx_alloc(c, (void**)&c->d_dist, max_sources * c->V * 8))) return fail(st);
   if ((st = ctx_alloc(c, (void**)&c->d_settled, max_sources * c->V * 4))) return fail(st);
   if ((st = ctx_alloc(c, (void**)&c->d_parent, max_sources * c->V * 4))) return fail(st);
   if ((st = ctx_alloc(c, (void**)&c->d_src, max_sources * 4))) return fail(st);
-  if (c->lane &&
-      (st = ctx_alloc(c, (void**)&c->d_save,
+  if ((st = ctx_alloc(c, (void**)&c->d_save,
                       max_sources * std::max(bank_save_bytes_nw(c->bank_nw), sizeof(MultiImage)))))
     return fail(st);
   c->heaps.resize(max_sources);
@@ -1244,7 +1140,7 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
   {
     DevHeap M;
     M.measure = true;
-    if (c->lane) M.base1 = base1, M.bank = true;
+    M.base1 = base1, M.bank = true;
     init_heap(M, c->d, c->cap0, bc, c->nt, std::max<u32>(c->V, 1), 0, nlev, c->d_heaps);
     per_heap = M.measured;
   }
@@ -1252,7 +1148,7 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
   if ((st = ctx_alloc(c, (void**)&arena, per_heap * max_sources))) return fail(st);
   for (u64 i = 0; i < max_sources; ++i) {
     DevHeap& H = c->heaps[i];
-    if (c->lane) H.base1 = base1, H.bank = true;
+    H.base1 = base1, H.bank = true;
     H.arena = arena + per_heap * i;
     H.arena_cap = per_heap;
     st = init_heap(H, c->d, c->cap0, bc, c->nt, std::max<u32>(c->V, 1), 0, nlev, c->d_heaps + i,
@@ -1295,6 +1191,8 @@ pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n
     return set_err(PBH_PRECONDITION, "n_sources out of range");
   for (u64 i = 0; i < n_sources; ++i)
     if (sources[i] >= c->V) return set_err(PBH_PRECONDITION, "par_dijkstra: source out of range");
+  if (!c->graph_ok)
+    return set_err(PBH_PRECONDITION, "par_dijkstra: the context holds no valid graph (a failed load_graph)");
   CK(cudaSetDevice(c->device));
   pbh_status st = ctx_reset(c, n_sources);
   if (st) return st;
@@ -1307,15 +1205,11 @@ pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n
       CK(launch_sssp_multi(c->stream, (u32)n_sources, c->d_heaps, c->d_off, c->d_tgt, c->d_w,
                            c->d_mwo, c->d_mwi, c->V, c->d_src, c->d_dist, c->d_settled, c->d_sst,
                            c->d_save, c->max_deg, (u32)std::min<u64>(c->d, 0xffffffffu)));
-    } else if (c->lane) {
+    } else {
       CK(launch_sssp_bank_nw(c->bank_nw, c->stream, (u32)n_sources, c->d_heaps, c->d_off,
                              c->d_tgt, c->d_w, c->V, c->d_src, c->d_dist, c->d_settled, c->d_sst,
                              c->d_save, dag_mode ? 1 : 0, c->max_deg,
                              (u32)std::min<u64>(c->d, 0xffffffffu)));
-    } else {
-      CK(launch_sssp_nt(c->nt, c->layout, c->stream, (u32)n_sources, c->d_heaps, c->d_off,
-                        c->d_tgt, c->d_w, c->V, c->d_src, c->d_dist, c->d_settled, c->d_sst,
-                        dag_mode ? 1 : 0, c->max_deg));
     }
     CK(cudaEventRecord(c->ev1, c->stream));
     CK(cudaMemcpyAsync(hs.data(), c->d_sst, n_sources * sizeof(SsspState), cudaMemcpyDeviceToHost,
@@ -1364,9 +1258,6 @@ pbh_status pbh_sssp_ctx_run(pbh_sssp_ctx* c, const uint32_t* sources, uint64_t n
               "pass-top(cold) %.0f gathers+binsearch %.0f atomics+apply+exchange %.0f tail %.0f loop %.0f\n",
               s0.phase[0] / r, s0.phase[1] / r, s0.phase[2] / r, s0.phase[3] / r, s0.phase[4] / r,
               s0.phase[5] / r, s0.phase[6] / r, s0.phase[7] / r);
-    if (!c->lane)
-      fprintf(stderr, "phases cyc/round (cta): %.0f %.0f %.0f %.0f %.0f\n", s0.phase[0] / r,
-              s0.phase[1] / r, s0.phase[2] / r, s0.phase[3] / r, s0.phase[4] / r);
   }
   return PBH_OK;
 }
@@ -1385,21 +1276,12 @@ pbh_status pbh_sssp_ctx_fetch(pbh_sssp_ctx* c, uint64_t slot, uint64_t* dist, ui
     CK(cudaMemcpy(settled, c->d_settled + slot * c->V, s.n_settled * 4, cudaMemcpyDeviceToHost));
   if (n_settled) *n_settled = s.n_settled;
   if (rounds) *rounds = s.rounds;
-  if (ops) {
-    if (c->fast) {
-      *ops = s.ops;
-    } else {
-      u64 o = 0;
-      CK(cudaMemcpy(&o, &c->heaps[slot].dev->ops, 8, cudaMemcpyDeviceToHost));
-      *ops = o;
-    }
-  }
+  if (ops) *ops = s.ops;
   return PBH_OK;
 }
 
 pbh_status pbh_sssp_ctx_set_mode(pbh_sssp_ctx* c, int mode) {
   if (!c || (mode != 0 && mode != 1)) return set_err(PBH_PRECONDITION, "bad mode");
-  if (mode == 1 && !c->lane) return set_err(PBH_PRECONDITION, "threshold mode needs the banked engine");
   CK(cudaSetDevice(c->device));
   if (mode == 1 && !c->d_mwo) {
     pbh_status st;
@@ -1422,22 +1304,49 @@ pbh_status pbh_sssp_ctx_load_graph(pbh_sssp_ctx* c, const pbh_csr* g) {
   if (!c || !g) return set_err(PBH_PRECONDITION, "bad arguments");
   if (g->vertex_count != c->V || g->edge_count != c->E)
     return set_err(PBH_PRECONDITION, "load_graph: vertex/edge count differs from the context");
+  if (!g->offsets || (c->E && (!g->targets || !g->weights)))
+    return set_err(PBH_PRECONDITION, "load_graph: null CSR array");
   CK(cudaSetDevice(c->device));
+  // The shape check (max out-degree, which sizes the heaps, sssp.cpp:24-26)
+  // runs on the NEW graph before anything in the context changes: device
+  // arrays are checked in place, host offsets on the host (8 B per vertex).
+  const bool dev_src = device_accessible(g->offsets) && (!c->E || (device_accessible(g->targets) &&
+                                                                    device_accessible(g->weights)));
+  pbh_status st;
+  if (dev_src) {
+    CsrCheck chk{};
+    if ((st = csr_check(c->stream, c->d_chk, g->offsets, g->targets, g->weights, c->V, c->E, &chk)))
+      return st;
+    if ((st = csr_precondition(chk, "load_graph"))) return st;
+    if ((u32)chk.max_deg != c->max_deg)
+      return set_err(PBH_PRECONDITION, "load_graph: max out-degree differs from the context");
+  } else {
+    const u64* o = g->offsets;
+    if (o[0] != 0 || o[c->V] != c->E)
+      return set_err(PBH_PRECONDITION, "load_graph: graph: inconsistent array sizes");
+    u64 md = 0;
+    for (u64 u = 0; u < c->V; ++u) {
+      if (o[u] > o[u + 1]) return set_err(PBH_PRECONDITION, "load_graph: graph: offsets not monotone");
+      md = std::max<u64>(md, o[u + 1] - o[u]);
+    }
+    if ((u32)md != c->max_deg)
+      return set_err(PBH_PRECONDITION, "load_graph: max out-degree differs from the context");
+  }
   CK(cudaMemcpyAsync(c->d_off, g->offsets, ((u64)c->V + 1) * 8, cudaMemcpyDefault, c->stream));
   if (c->E) {
     CK(cudaMemcpyAsync(c->d_tgt, g->targets, c->E * 4, cudaMemcpyDefault, c->stream));
     CK(cudaMemcpyAsync(c->d_w, g->weights, c->E * 4, cudaMemcpyDefault, c->stream));
   }
-  // the derived heap shapes depend on the max out-degree (sssp.cpp:24-26)
-  CK(cudaMemsetAsync(c->d_md, 0, 8, c->stream));
-  k_max_degree<<<std::max<u32>(1, std::min<u32>(1184, (c->V + 255) / 256)), 256, 0, c->stream>>>(
-      c->d_off, c->V, c->d_md);
-  g_launches++;
-  unsigned long long md = 0;
-  CK(cudaMemcpyAsync(&md, c->d_md, 8, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  if ((u32)md != c->max_deg)
-    return set_err(PBH_PRECONDITION, "load_graph: max out-degree differs from the context");
+  if (!dev_src) {
+    // host targets are range-checked on the resident copy; a bad graph
+    // leaves the context refusing to run until a valid one is loaded
+    c->graph_ok = false;
+    CsrCheck chk{};
+    if ((st = csr_check(c->stream, c->d_chk, c->d_off, c->d_tgt, c->d_w, c->V, c->E, &chk)))
+      return st;
+    if ((st = csr_precondition(chk, "load_graph"))) return st;
+  }
+  c->graph_ok = true;
   if (c->d_mwo) {  // threshold mode's per-vertex minimum weights
     CK(cudaMemsetAsync(c->d_mwi, 0xff, (u64)c->V * 4, c->stream));
     int sms = 0;
@@ -1446,8 +1355,8 @@ pbh_status pbh_sssp_ctx_load_graph(pbh_sssp_ctx* c, const pbh_csr* g) {
                                                   c->d_mwi);
     g_launches++;
     CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(c->stream));
   }
+  CK(cudaStreamSynchronize(c->stream));
   return PBH_OK;
 }
 
@@ -1544,6 +1453,20 @@ pbh_status pbh_bellman_ford(const pbh_csr* g, uint32_t source, int device, uint6
   if (E) {
     cudaMemcpyAsync(d_tgt, g->targets, E * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(d_w, g->weights, E * 4, cudaMemcpyHostToDevice, st);
+  }
+  {
+    CsrCheck* d_chk = nullptr;
+    if (!dalloc((void**)&d_chk, sizeof(CsrCheck))) {
+      cudaStreamDestroy(st);
+      return fin(set_err(PBH_OOM, "bellman_ford: device allocation failed"));
+    }
+    CsrCheck chk{};
+    pbh_status cs = csr_check(st, d_chk, d_off, d_tgt, d_w, (u32)V, E, &chk);
+    if (!cs) cs = csr_precondition(chk, "bellman_ford");
+    if (cs) {
+      cudaStreamDestroy(st);
+      return fin(cs);
+    }
   }
   cudaMemsetAsync(d_dist, 0xff, V * 8, st);
   cudaMemsetAsync(d_dist + source, 0, 8, st);
@@ -1703,6 +1626,138 @@ pbh_status pbh_sssp_multi_device(const pbh_csr* g, const uint32_t* sources, uint
   for (int r = 0; r < n_devices; ++r)
     if (res[r]) return set_err(res[r], msg[r]);
   if (device_ms) *device_ms = *std::max_element(ms.begin(), ms.end());
+  return PBH_OK;
+}
+
+pbh_status pbh_validate_graph(const pbh_csr* g, int device) {
+  if (!g || !g->offsets || (g->edge_count && (!g->targets || !g->weights)))
+    return set_err(PBH_PRECONDITION, "validate_graph: null CSR array");
+  CK(cudaSetDevice(device));
+  const u64 V = g->vertex_count, E = g->edge_count;
+  const bool dev_src = device_accessible(g->offsets) &&
+                       (!E || (device_accessible(g->targets) && device_accessible(g->weights)));
+  std::vector<void*> mem;
+  auto fin = [&](pbh_status s) {
+    for (void* p : mem) cudaFree(p);
+    return s;
+  };
+  const u64* off = g->offsets;
+  const u32 *tgt = g->targets, *w = g->weights;
+  cudaStream_t s = nullptr;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  auto up = [&](const void* src, size_t bytes, void** dst) -> bool {
+    if (cudaMalloc(dst, bytes ? bytes : 16) != cudaSuccess) return false;
+    mem.push_back(*dst);
+    return !bytes || cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess;
+  };
+  if (!dev_src) {
+    // host arrays: staged through device memory for the one-pass check
+    if (!up(g->offsets, (V + 1) * 8, (void**)&off) || !up(g->targets, E * 4, (void**)&tgt) ||
+        !up(g->weights, E * 4, (void**)&w)) {
+      cudaStreamDestroy(s);
+      return fin(set_err(PBH_OOM, "validate_graph: staging allocation failed"));
+    }
+  }
+  CsrCheck* d_chk = nullptr;
+  if (cudaMalloc(&d_chk, sizeof(CsrCheck)) != cudaSuccess) {
+    cudaStreamDestroy(s);
+    return fin(set_err(PBH_OOM, "validate_graph: allocation failed"));
+  }
+  mem.push_back(d_chk);
+  CsrCheck chk{};
+  pbh_status st = csr_check(s, d_chk, off, tgt, w, (u32)V, E, &chk);
+  cudaStreamDestroy(s);
+  if (st) return fin(st);
+  if (chk.sizes_bad || chk.first != ~0ull) return fin(set_err(PBH_INVARIANT, csr_message(chk)));
+  return fin(PBH_OK);
+}
+
+pbh_status pbh_csr_max_out_degree(const pbh_csr* g, int device, uint32_t* out) {
+  if (!g || !out || !g->offsets) return set_err(PBH_PRECONDITION, "bad arguments");
+  if (!device_accessible(g->offsets)) {
+    u64 best = 0;
+    for (u64 u = 0; u < g->vertex_count; ++u)
+      best = std::max<u64>(best, g->offsets[u + 1] - g->offsets[u]);
+    *out = (u32)best;
+    return PBH_OK;
+  }
+  CK(cudaSetDevice(device));
+  if (g->edge_count && (!g->targets || !g->weights))
+    return set_err(PBH_PRECONDITION, "null CSR array");
+  CsrCheck* d_chk = nullptr;
+  CK(cudaMalloc(&d_chk, sizeof(CsrCheck)));
+  cudaStream_t s = nullptr;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  CsrCheck chk{};
+  pbh_status st = csr_check(s, d_chk, g->offsets, g->targets, g->weights, g->vertex_count,
+                            g->edge_count, &chk);
+  cudaStreamDestroy(s);
+  cudaFree(d_chk);
+  if (st) return st;
+  *out = (u32)chk.max_deg;
+  return PBH_OK;
+}
+
+pbh_status pbh_sssp_ctx_gather(pbh_sssp_ctx* c, uint64_t first_slot, uint64_t n_slots,
+                               uint64_t* dist_dst, uint32_t* parent_dst) {
+  if (!c || first_slot + n_slots > c->n_last || (!dist_dst && !parent_dst))
+    return set_err(PBH_PRECONDITION, "gather: bad slot range or no destination");
+  CK(cudaSetDevice(c->device));
+  const u64 V = c->V;
+  // cudaMemcpyDefault: host, local device, peer device (NVLink), or an
+  // IPC-mapped buffer of another process (pbh_ipc_open)
+  if (dist_dst)
+    CK(cudaMemcpyAsync(dist_dst, c->d_dist + first_slot * V, n_slots * V * 8, cudaMemcpyDefault,
+                       c->stream));
+  if (parent_dst)
+    CK(cudaMemcpyAsync(parent_dst, c->d_parent + first_slot * V, n_slots * V * 4,
+                       cudaMemcpyDefault, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return PBH_OK;
+}
+
+pbh_status pbh_device_alloc(int device, uint64_t bytes, void** ptr) {
+  if (!ptr) return set_err(PBH_PRECONDITION, "null output pointer");
+  *ptr = nullptr;
+  CK(cudaSetDevice(device));
+  CK(cudaMalloc(ptr, bytes ? bytes : 16));
+  return PBH_OK;
+}
+
+pbh_status pbh_device_free(int device, void* ptr) {
+  CK(cudaSetDevice(device));
+  if (ptr) CK(cudaFree(ptr));
+  return PBH_OK;
+}
+
+pbh_status pbh_copy(void* dst, const void* src, uint64_t bytes) {
+  if (!bytes) return PBH_OK;
+  if (!dst || !src) return set_err(PBH_PRECONDITION, "null pointer");
+  CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
+  return PBH_OK;
+}
+
+pbh_status pbh_ipc_export(void* dev_ptr, uint8_t handle[64]) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  if (!dev_ptr || !handle) return set_err(PBH_PRECONDITION, "null pointer");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, dev_ptr));
+  std::memcpy(handle, &h, 64);
+  return PBH_OK;
+}
+
+pbh_status pbh_ipc_open(const uint8_t handle[64], int device, void** ptr) {
+  if (!handle || !ptr) return set_err(PBH_PRECONDITION, "null pointer");
+  CK(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  CK(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return PBH_OK;
+}
+
+pbh_status pbh_ipc_close(int device, void* ptr) {
+  CK(cudaSetDevice(device));
+  if (ptr) CK(cudaIpcCloseMemHandle(ptr));
   return PBH_OK;
 }
 

@@ -202,6 +202,7 @@ struct GridJob {
 // fills the fields and zeroes the counters before posting.
 constexpr u32 kSortChunk = 2048;  // elements per CTA-sorted chunk
 constexpr u32 kBigBatch = 8192;   // batches at least this large go to the grid
+constexpr u32 kMaxBatch = 1u << 26;  // largest batch (size of the grid path's staging buffers)
 #ifndef PBH_POLL_MAX_NS
 #define PBH_POLL_MAX_NS 64
 #endif

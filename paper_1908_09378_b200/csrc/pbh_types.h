@@ -72,6 +72,11 @@ typedef struct {
   uint64_t* g_cp;
   uint64_t* g_co;
   uint32_t* g_cs;
+  // deletes of values beyond the index (absent values: no-ops) remembered so
+  // that a later index growth marks them DEAD, as the reference's
+  // shadow_dead_ set does (bucket_heap.cpp:55-58,113-125)
+  uint32_t* oor_del;
+  uint32_t oor_n, oor_cap;
 } pbh_heap_dev;
 
 // Op stream (trace_format.hpp:16-33) in device memory.

@@ -100,8 +100,16 @@ class Engine:
         v, p = e
         raise_for(_lib.lib().pbh_heap_update(self._h, int(v), int(p)))
 
-    def bulk_update(self, batch):
-        if isinstance(batch, tuple) and len(batch) == 2 and hasattr(batch[0], "__len__"):
+    def bulk_update(self, batch=None, *, values=None, priorities=None):
+        """Engine::bulk_update (engine.cpp:95-98). ``batch`` is a sequence of
+        Elements or (value, priority) pairs; columnar input is given by
+        keyword (``values=``, ``priorities=``) or as a pair of numpy arrays."""
+        if values is not None or priorities is not None:
+            if batch is not None or values is None or priorities is None:
+                raise TypeError("bulk_update: pass either a batch or values= and priorities=")
+            vals, prios = values, priorities
+        elif (isinstance(batch, tuple) and len(batch) == 2 and isinstance(batch[0], np.ndarray)
+              and isinstance(batch[1], np.ndarray)):
             vals, prios = batch
         else:
             pairs = [tuple(e) for e in batch]  # Element or (value, priority)

@@ -158,6 +158,14 @@ class SsspContext:
         raise_for(_lib.lib().pbh_sssp_ctx_load_graph(self._h, C.byref(cs)))
         self.g = g
 
+    def gather(self, first_slot: int, n_slots: int, dist_addr: int, parent_addr: int = 0):
+        """pbh_sssp_ctx_gather: copy the dist / parent rows of slots
+        [first_slot, first_slot + n_slots) to raw addresses (host, this
+        device, a peer device or an IPC-mapped buffer of another process)."""
+        raise_for(_lib.lib().pbh_sssp_ctx_gather(self._h, first_slot, n_slots,
+                                                 C.c_void_p(dist_addr or None),
+                                                 C.c_void_p(parent_addr or None)))
+
     def fetch_into(self, slot, dist, parent=None):
         """D2H of one source's dist (u64[V]) and parent (u32[V]) into
         caller-owned (e.g. page-locked) arrays."""
@@ -194,6 +202,23 @@ class SsspContext:
     __del__ = close
 
 
+def validate_graph(g, device: int = 0):
+    """validate_graph (graphs.hpp:23; graphs.cpp:55-72) as one device pass:
+    raises InvariantError with the reference's message."""
+    g = g if type(g).__name__ == "DeviceCsr" else CsrGraph.of(g)
+    cs = g.c_struct()
+    raise_for(_lib.lib().pbh_validate_graph(C.byref(cs), device))
+
+
+def max_out_degree(g, device: int = 0) -> int:
+    """CsrGraph::max_out_degree (graphs.hpp:18; graphs.cpp:47-53)."""
+    g = g if type(g).__name__ == "DeviceCsr" else CsrGraph.of(g)
+    cs = g.c_struct()
+    out = C.c_uint32()
+    raise_for(_lib.lib().pbh_csr_max_out_degree(C.byref(cs), device, C.byref(out)))
+    return out.value
+
+
 def distance_checksum(dist) -> int:
     """sssp.cpp:174-183."""
     d = np.ascontiguousarray(dist, dtype=np.uint64)
@@ -208,11 +233,55 @@ def distances_to_csv(dist) -> str:
     return "\n".join(out) + "\n"
 
 
-def validate_parent_tree(g, source, dist, parent) -> str | None:
+def certify_distances(g, source, dist, chunk=1 << 24) -> str | None:
+    """Optimality certificate for ``dist`` (independent of any solver): the
+    source is at 0 and no edge can still relax, i.e. for every edge (u, v, w)
+    with dist[u] finite, dist[u] + w >= dist[v] (and dist[v] finite). With a
+    valid parent tree (every reached vertex at the end of a tight edge path
+    from the source) this proves dist is the exact shortest-path distance.
+    Returns None when it holds, else a message. Chunked over edges."""
+    g = CsrGraph.of(g)
+    off = np.asarray(g.offsets, np.uint64)
+    tgt = np.asarray(g.targets, np.uint32)
+    w = np.asarray(g.weights, np.uint64)
+    dist = np.asarray(dist, np.uint64)
+    V = g.vertex_count
+    if dist[source] != 0:
+        return "dist[source] != 0"
+    inf = np.uint64(K_INF_DIST)
+    deg = np.diff(off).astype(np.int64)
+    E = len(tgt)
+    for b in range(0, E, chunk):
+        e = min(E, b + chunk)
+        # source vertex of each edge in [b, e)
+        u0 = int(np.searchsorted(off, b, side="right")) - 1
+        u1 = int(np.searchsorted(off, e - 1, side="right")) - 1
+        us = np.repeat(np.arange(u0, u1 + 1, dtype=np.int64), deg[u0:u1 + 1])
+        first = b - int(off[u0])
+        us = us[first:first + (e - b)]
+        du = dist[us]
+        fin = du != inf
+        dv = dist[tgt[b:e]]
+        # fin & (dv == inf): a reachable target never reached
+        if np.any(fin & (dv == inf)):
+            return "reachable vertex left at infinity"
+        cand = du[fin] + w[b:e][fin]
+        if np.any(cand < du[fin]):
+            return "distance overflow"
+        if np.any(cand < dv[fin]):
+            i = int(np.nonzero(cand < dv[fin])[0][0])
+            return f"edge can still relax (edge {b + int(np.nonzero(fin)[0][i])})"
+    del V
+    return None
+
+
+def validate_parent_tree(g, source, dist, parent, optimal=False) -> str | None:
     """Shortest-path-tree validator: for every reached v != s,
     parent[v] has an edge to v with dist[v] == dist[parent] + w; the source is
-    its own parent; unreachable vertices have no parent. Returns None when
-    valid, else a message."""
+    its own parent; unreachable vertices have no parent. With ``optimal``,
+    also the certificate of :func:`certify_distances` (no edge can relax), so
+    a consistent-but-wrong dist vector fails. Returns None when valid, else a
+    message."""
     g = CsrGraph.of(g)
     off = np.asarray(g.offsets, np.uint64)
     tgt = np.asarray(g.targets, np.uint32)
@@ -249,6 +318,8 @@ def validate_parent_tree(g, source, dist, parent) -> str | None:
         return "parent edge missing"
     if not np.all(dist[par] + w[a] == dist[vs]):
         return "dist[v] != dist[parent] + w"
+    if optimal:
+        return certify_distances(g, source, dist)
     return None
 
 
