@@ -1,7 +1,7 @@
 /* pbh-b200 — C-ABI of the B200-native parBucketHeap hot path.
  *
  * Drop-in boundary for the reference's priority-queue + SSSP API
- * (/root/reference/proj/include/pbh/*.hpp). Plain pointers and sizes only;
+ * (/root/reference/proj/include/pbh/ headers). Plain pointers and sizes only;
  * no torch or CUDA types. Every entry point returns a pbh_status; the message
  * of the last failure on the calling thread is pbh_last_error().
  *

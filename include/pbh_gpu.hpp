@@ -7,15 +7,19 @@
 //        InvariantError, TraceError          (proj/include/pbh/error.hpp:9-30)
 //   pbh::EngineConfig, Metrics, Engine       (proj/include/pbh/engine.hpp:17-103)
 //   pbh::TraceOp / Trace / OpKind            (proj/include/pbh/trace_format.hpp:16-33)
-//   pbh::CsrGraph, SsspResult, kInfDist,
-//        par_dijkstra, distance_checksum     (proj/include/pbh/graphs.hpp:11-20,
-//                                             proj/include/pbh/sssp.hpp:13-48)
+//   pbh::CsrGraph (+ max_out_degree, ==),
+//        validate_graph                      (proj/include/pbh/graphs.hpp:11-23)
+//   pbh::SsspResult, kInfDist, par_dijkstra,
+//        bellman_ford, distances_to_csv,
+//        distance_checksum                   (proj/include/pbh/sssp.hpp:13-48)
 // inside namespace pbh::gpu. A caller switches with
 //     namespace pbh = ::pbh::gpu;   (or `using namespace pbh::gpu;`)
 // and links libpbh_gpu.so; every operation then runs on the B200.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <numeric>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -223,7 +227,30 @@ struct CsrGraph {
   std::vector<std::uint64_t> offsets;
   std::vector<std::uint32_t> targets;
   std::vector<std::uint32_t> weights;
+
+  pbh_csr c_view() const {
+    return pbh_csr{vertex_count, edge_count, offsets.data(), targets.data(), weights.data()};
+  }
+  /// graphs.hpp:18 (graphs.cpp:47-53).
+  std::uint32_t max_out_degree() const {
+    const pbh_csr c = c_view();
+    std::uint32_t d = 0;
+    detail::check(pbh_csr_max_out_degree(&c, 0, &d));
+    return d;
+  }
+  bool operator==(const CsrGraph&) const = default;  // graphs.hpp:19
 };
+
+/// graphs.hpp:23 (graphs.cpp:55-72), one device pass: throws InvariantError
+/// with the reference's message. Array-size mismatches of the vectors
+/// themselves are caught here before the call.
+inline void validate_graph(const CsrGraph& g, int device = 0) {
+  if (g.offsets.size() != static_cast<std::size_t>(g.vertex_count) + 1 ||
+      g.targets.size() != g.edge_count || g.weights.size() != g.edge_count)
+    throw InvariantError("graph: inconsistent array sizes");
+  const pbh_csr c = g.c_view();
+  detail::check(pbh_validate_graph(&c, device));
+}
 
 struct SsspResult {
   std::vector<std::uint64_t> dist;
@@ -235,7 +262,7 @@ struct SsspResult {
 
 inline SsspResult par_dijkstra(const CsrGraph& g, std::uint32_t source, EngineConfig cfg,
                                bool dag_mode = false) {
-  pbh_csr c{g.vertex_count, g.edge_count, g.offsets.data(), g.targets.data(), g.weights.data()};
+  const pbh_csr c = g.c_view();
   SsspResult r;
   r.dist.resize(g.vertex_count);
   r.parent.resize(g.vertex_count);
@@ -246,6 +273,38 @@ inline SsspResult par_dijkstra(const CsrGraph& g, std::uint32_t source, EngineCo
                          &r.metrics.ops));
   r.settled_order.resize(ns);
   return r;
+}
+
+/// sssp.hpp:37 (sssp.cpp:99-129) as the device frontier sweep: exact
+/// distances; settled_order = reached vertices in (dist, vertex) order, as
+/// the reference's stable sort by distance reports them (sssp.cpp:122-127);
+/// rounds = frontier iterations (the reference counts full sweeps).
+inline SsspResult bellman_ford(const CsrGraph& g, std::uint32_t source, int device = 0) {
+  const pbh_csr c = g.c_view();
+  SsspResult r;
+  r.dist.resize(g.vertex_count);
+  r.parent.resize(g.vertex_count);
+  std::uint64_t scanned = 0;
+  double ms = 0;
+  detail::check(pbh_bellman_ford(&c, source, device, r.dist.data(), r.parent.data(), &r.rounds,
+                                 &scanned, &ms));
+  for (std::uint32_t v = 0; v < g.vertex_count; ++v)
+    if (r.dist[v] != kInfDist) r.settled_order.push_back(v);
+  std::stable_sort(r.settled_order.begin(), r.settled_order.end(),
+                   [&](std::uint32_t a, std::uint32_t b) { return r.dist[a] < r.dist[b]; });
+  return r;
+}
+
+/// sssp.hpp:43 (sssp.cpp:159-172): header "vertex,dist", "inf" if unreachable.
+inline std::string distances_to_csv(const std::vector<std::uint64_t>& dist) {
+  std::string out = "vertex,dist\n";
+  for (std::size_t v = 0; v < dist.size(); ++v) {
+    out += std::to_string(v);
+    out += ',';
+    out += dist[v] == kInfDist ? std::string("inf") : std::to_string(dist[v]);
+    out += '\n';
+  }
+  return out;
 }
 
 inline std::uint64_t distance_checksum(const std::vector<std::uint64_t>& dist) {

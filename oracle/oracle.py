@@ -255,6 +255,8 @@ def ref():
         L.ref_trace_sizes.argtypes = [V, U64P, U64P, U64P]
         L.ref_trace_export.argtypes = [V, U8P, U64P, U32P, U64P]
         L.ref_trace_free.argtypes = [V]
+        L.ref_trace_load_text.restype = V
+        L.ref_trace_load_text.argtypes = [C.c_char_p, U64P]
         L.ref_run_oracle.argtypes = [V, U32P, U64P, U64P]
         L.ref_engine_run_trace.argtypes = [V, C.c_uint64, C.c_uint64, C.c_int, U32P, U64P, U64P,
                                            U64P, U64P]
@@ -288,6 +290,26 @@ class RefError(RuntimeError):
 def ref_gen_legal_trace(n_ops, d, seed):
     L = ref()
     h = L.ref_trace_gen_legal(n_ops, d, seed)
+    n, m, x = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    L.ref_trace_sizes(h, C.byref(n), C.byref(m), C.byref(x))
+    kinds = np.zeros(n.value, np.uint8)
+    offs = np.zeros(n.value + 1, np.uint64)
+    vals = np.zeros(max(m.value, 1), np.uint32)
+    prios = np.zeros(max(m.value, 1), np.uint64)
+    L.ref_trace_export(h, _p(kinds, U8P), _p(offs, U64P), _p(vals, U32P), _p(prios, U64P))
+    L.ref_trace_free(h)
+    return Trace(kinds, offs, vals[:m.value], prios[:m.value])
+
+
+def ref_load_text(path):
+    """The reference's load_trace (trace_format.cpp:34-98). Returns a Trace,
+    or raises RefError(op_index=...) with the reference's message."""
+    L = ref()
+    failed = C.c_uint64()
+    h = L.ref_trace_load_text(str(path).encode(), C.byref(failed))
+    if not h:
+        raise RefError(4, L.ref_last_error().decode(),
+                       None if failed.value == 2 ** 64 - 1 else failed.value)
     n, m, x = C.c_uint64(), C.c_uint64(), C.c_uint64()
     L.ref_trace_sizes(h, C.byref(n), C.byref(m), C.byref(x))
     kinds = np.zeros(n.value, np.uint8)

@@ -138,6 +138,22 @@ void ref_trace_export(void* h, std::uint8_t* kinds, std::uint64_t* offsets, std:
 
 void ref_trace_free(void* h) { delete static_cast<RefTrace*>(h); }
 
+/// load_trace (trace_format.cpp:93-98): nullptr on failure with the message
+/// in ref_last_error() and the TraceError op index in *failed_op.
+void* ref_trace_load_text(const char* path, std::uint64_t* failed_op) {
+  *failed_op = ~std::uint64_t{0};
+  try {
+    return new RefTrace{load_trace(path)};
+  } catch (const TraceError& e) {
+    g_err = e.what();
+    *failed_op = e.op_index;
+    return nullptr;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
 /// run_oracle: the reference's model PQ (tests/oracle.hpp:55-75).
 int ref_run_oracle(void* h, std::uint32_t* out_v, std::uint64_t* out_p, std::uint64_t* n_out) {
   return guarded([&] {

@@ -2,12 +2,17 @@
 // a packed binary form with a streaming chunk reader. See include/pbh_trace_io.h.
 #include "../../include/pbh_trace_io.h"
 
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <charconv>
 #include <cstdio>
 #include <cstring>
-#include <fstream>
-#include <limits>
-#include <sstream>
+#include <memory>
 #include <string>
+#include <string_view>
 #include <vector>
 
 #include "../../include/pbh_gpu.h"
@@ -36,31 +41,90 @@ int fail(int st, const std::string& m) {
 
 uint64_t pad8(uint64_t x) { return (x + 7) & ~uint64_t(7); }
 
-struct ParseError {
-  uint64_t op;
-  std::string msg;
-};
-
-// trace_format.cpp:13-23
-uint64_t parse_number(std::istringstream& line, uint64_t op, uint64_t line_no, const char* what,
-                      uint64_t max) {
-  uint64_t x = 0;
-  if (!(line >> x))
-    throw ParseError{op, "line " + std::to_string(line_no) + ": missing or bad " + what};
-  if (x > max) throw ParseError{op, "line " + std::to_string(line_no) + ": " + what + " out of range"};
-  return x;
-}
-
-void require_line_end(std::istringstream& line, uint64_t op, uint64_t line_no) {
-  std::string rest;
-  if (line >> rest) throw ParseError{op, "line " + std::to_string(line_no) + ": trailing tokens"};
-}
-
 bool write_all(FILE* f, const void* p, size_t n) { return n == 0 || fwrite(p, 1, n, f) == n; }
 bool write_pad(FILE* f, size_t n) {
   static const uint8_t z[8] = {0};
   return n == 0 || fwrite(z, 1, n, f) == n;
 }
+
+// ---------------------------------------------------------------- text reader
+// The whole file is mapped read-only and scanned once: lines are split with
+// memchr, '#' cuts a line, and tokens are maximal runs of non-space bytes.
+// Numbers follow the stream-extraction rules the reference relies on
+// (`line >> u64`, trace_format.cpp:13-30): leading blanks skipped, an
+// optional sign, at least one digit, overflow is a bad number, "-n" wraps
+// modulo 2^64, and characters after the digits stay for the next read.
+
+struct MappedFile {
+  const char* data = nullptr;
+  size_t size = 0;
+  std::vector<char> copy;  // fallback when mmap is unavailable (pipes, empty files)
+  void* map = nullptr;
+  bool open(const char* path) {
+    const int fd = ::open(path, O_RDONLY);
+    if (fd < 0) return false;
+    struct stat st {};
+    if (fstat(fd, &st) == 0 && S_ISREG(st.st_mode) && st.st_size > 0) {
+      map = mmap(nullptr, (size_t)st.st_size, PROT_READ, MAP_PRIVATE, fd, 0);
+      if (map != MAP_FAILED) {
+        madvise(map, (size_t)st.st_size, MADV_SEQUENTIAL);
+        data = static_cast<const char*>(map);
+        size = (size_t)st.st_size;
+        ::close(fd);
+        return true;
+      }
+      map = nullptr;
+    }
+    char buf[1 << 16];
+    for (ssize_t n; (n = ::read(fd, buf, sizeof buf)) > 0;) copy.insert(copy.end(), buf, buf + n);
+    ::close(fd);
+    data = copy.data();
+    size = copy.size();
+    return true;
+  }
+  ~MappedFile() {
+    if (map) munmap(map, size);
+  }
+};
+
+inline bool is_blank(char ch) {
+  return ch == ' ' || ch == '\t' || ch == '\r' || ch == '\v' || ch == '\f';
+}
+
+struct LineScanner {
+  const char* p;
+  const char* end;
+  void skip_blanks() {
+    while (p < end && is_blank(*p)) ++p;
+  }
+  // next maximal non-blank run; empty when the line is exhausted
+  std::string_view token() {
+    skip_blanks();
+    const char* b = p;
+    while (p < end && !is_blank(*p)) ++p;
+    return {b, size_t(p - b)};
+  }
+  bool at_end() {
+    skip_blanks();
+    return p == end;
+  }
+  bool number(uint64_t* out) {
+    skip_blanks();
+    bool neg = false;
+    if (p < end && (*p == '+' || *p == '-')) neg = *p++ == '-';
+    uint64_t x = 0;
+    const auto r = std::from_chars(p, end, x, 10);
+    if (r.ec != std::errc()) return false;  // no digits, or overflow
+    p = r.ptr;
+    *out = neg ? uint64_t(0) - x : x;
+    return true;
+  }
+};
+
+struct TraceSyntax {
+  uint64_t op;
+  std::string msg;
+};
 
 }  // namespace
 
@@ -72,68 +136,73 @@ int pbh_trace_load_text(const char* path, pbh_trace_buf** out, uint64_t* failed_
   if (!path || !out) return fail(PBH_PRECONDITION, "null argument");
   *out = nullptr;
   if (failed_op) *failed_op = ~0ull;
-  std::ifstream in(path);
-  if (!in) {
+  MappedFile f;
+  if (!f.open(path)) {
     if (failed_op) *failed_op = 0;
     return fail(PBH_TRACE, std::string("cannot open trace file: ") + path);
   }
-  auto* t = new pbh_trace_buf();
-  constexpr uint64_t kMaxValue = std::numeric_limits<uint32_t>::max();
-  constexpr uint64_t kMaxPrio = std::numeric_limits<uint64_t>::max();
-  std::string raw;
-  uint64_t line_no = 0;
+  std::unique_ptr<pbh_trace_buf> t(new pbh_trace_buf());
+  // value / priority ranges of Element (element.hpp:8-9); a batch holds at
+  // most 2^24 elements in the text format (trace_format.cpp:60)
+  const uint64_t value_max = 0xffffffffull, prio_max = ~0ull, batch_max = 1ull << 24;
+  const char* cur = f.data;
+  const char* const stop = f.data + f.size;
+  uint64_t line = 0;
   try {
-    while (std::getline(in, raw)) {
-      ++line_no;
-      const auto hash = raw.find('#');
-      if (hash != std::string::npos) raw.erase(hash);
-      std::istringstream line(raw);
-      std::string tag;
-      if (!(line >> tag)) continue;  // blank or comment-only line
+    while (cur < stop) {
+      const char* nl = static_cast<const char*>(std::memchr(cur, '\n', size_t(stop - cur)));
+      const char* eol = nl ? nl : stop;
+      ++line;
+      const char* hash = static_cast<const char*>(std::memchr(cur, '#', size_t(eol - cur)));
+      LineScanner s{cur, hash ? hash : eol};
+      cur = nl ? nl + 1 : stop;
+      const std::string_view tag = s.token();
+      if (tag.empty()) continue;
       const uint64_t op = t->kinds.size();
-      if (tag.size() != 1)
-        throw ParseError{op, "line " + std::to_string(line_no) + ": unknown op '" + tag + "'"};
-      switch (tag[0]) {
-        case 'U': {
-          const uint64_t v = parse_number(line, op, line_no, "value", kMaxValue);
-          const uint64_t p = parse_number(line, op, line_no, "priority", kMaxPrio);
-          require_line_end(line, op, line_no);
+      const std::string where = "line " + std::to_string(line) + ": ";
+      auto num = [&](const char* what, uint64_t max) {
+        uint64_t x = 0;
+        if (!s.number(&x)) throw TraceSyntax{op, where + "missing or bad " + what};
+        if (x > max) throw TraceSyntax{op, where + what + " out of range"};
+        return x;
+      };
+      auto done = [&] {
+        if (!s.at_end()) throw TraceSyntax{op, where + "trailing tokens"};
+      };
+      const char kind = tag.size() == 1 ? tag[0] : '?';
+      if (kind == 'U') {
+        const uint64_t v = num("value", value_max);
+        const uint64_t pr = num("priority", prio_max);
+        done();
+        t->values.push_back((uint32_t)v);
+        t->prios.push_back(pr);
+      } else if (kind == 'B') {
+        const uint64_t k = num("batch size", batch_max);
+        if (!k) throw TraceSyntax{op, where + "empty batch"};
+        for (uint64_t j = 0; j < k; ++j) {
+          const uint64_t v = num("value", value_max);
           t->values.push_back((uint32_t)v);
-          t->prios.push_back(p);
-          break;
+          t->prios.push_back(num("priority", prio_max));
         }
-        case 'B': {
-          const uint64_t k = parse_number(line, op, line_no, "batch size", 1u << 24);
-          if (k == 0) throw ParseError{op, "line " + std::to_string(line_no) + ": empty batch"};
-          for (uint64_t j = 0; j < k; ++j) {
-            t->values.push_back((uint32_t)parse_number(line, op, line_no, "value", kMaxValue));
-            t->prios.push_back(parse_number(line, op, line_no, "priority", kMaxPrio));
-          }
-          require_line_end(line, op, line_no);
-          break;
-        }
-        case 'E':
-          require_line_end(line, op, line_no);
-          break;
-        case 'D': {
-          const uint64_t v = parse_number(line, op, line_no, "value", kMaxValue);
-          require_line_end(line, op, line_no);
-          t->values.push_back((uint32_t)v);
-          t->prios.push_back(0);
-          break;
-        }
-        default:
-          throw ParseError{op, "line " + std::to_string(line_no) + ": unknown op '" + tag + "'"};
+        done();
+      } else if (kind == 'E') {
+        done();
+      } else if (kind == 'D') {
+        const uint64_t v = num("value", value_max);
+        done();
+        t->values.push_back((uint32_t)v);
+        t->prios.push_back(0);
+      } else {
+        throw TraceSyntax{op, where + "unknown op '" + std::string(tag) + "'"};
       }
-      t->kinds.push_back((uint8_t)tag[0]);
+      t->kinds.push_back((uint8_t)kind);
       t->offsets.push_back(t->values.size());
     }
-  } catch (const ParseError& e) {
-    delete t;
+  } catch (const TraceSyntax& e) {
     if (failed_op) *failed_op = e.op;
     return fail(PBH_TRACE, "op " + std::to_string(e.op) + ": " + e.msg);
   }
-  *out = t;
+  *out = t.release();
   return PBH_OK;
 }
 
@@ -157,30 +226,57 @@ int pbh_trace_save_text(const char* path, uint64_t n_ops, const uint8_t* kinds,
                         const uint64_t* offsets, const uint32_t* values,
                         const uint64_t* priorities) {
   if (!path || (n_ops && (!kinds || !offsets))) return fail(PBH_PRECONDITION, "null argument");
-  std::ofstream out(path);
-  if (!out) return fail(PBH_TRACE, std::string("cannot open trace file for writing: ") + path);
-  for (uint64_t i = 0; i < n_ops; ++i) {
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(PBH_TRACE, std::string("cannot open trace file for writing: ") + path);
+  // one line per op in the reference's text syntax (trace_format.hpp:16-33),
+  // formatted with to_chars into a 1 MiB block that is flushed when full
+  std::vector<char> blk(1 << 20);
+  size_t at = 0;
+  bool ok = true;
+  auto flush = [&] {
+    ok = ok && write_all(f, blk.data(), at);
+    at = 0;
+  };
+  auto room = [&](size_t n) {
+    if (at + n > blk.size()) flush();
+  };
+  auto put_u = [&](uint64_t x) {
+    room(24);
+    at = size_t(std::to_chars(blk.data() + at, blk.data() + blk.size(), x).ptr - blk.data());
+  };
+  auto put_c = [&](char ch) {
+    room(1);
+    blk[at++] = ch;
+  };
+  for (uint64_t i = 0; i < n_ops && ok; ++i) {
     const uint64_t b = offsets[i], e = offsets[i + 1];
-    switch (kinds[i]) {
-      case 'U':
-        out << "U " << values[b] << ' ' << priorities[b] << '\n';
-        break;
-      case 'B':
-        out << "B " << (e - b);
-        for (uint64_t j = b; j < e; ++j) out << ' ' << values[j] << ' ' << priorities[j];
-        out << '\n';
-        break;
-      case 'E':
-        out << "E\n";
-        break;
-      case 'D':
-        out << "D " << values[b] << '\n';
-        break;
-      default:
-        return fail(PBH_TRACE, "op " + std::to_string(i) + ": unknown op kind");
+    const uint8_t k = kinds[i];
+    if (k != 'U' && k != 'B' && k != 'E' && k != 'D') {
+      std::fclose(f);
+      return fail(PBH_TRACE, "op " + std::to_string(i) + ": unknown op kind");
     }
+    put_c((char)k);
+    if (k == 'B') {
+      put_c(' ');
+      put_u(e - b);
+    }
+    if (k != 'E') {
+      // U: one (value, priority); B: the batch; D: the value only
+      const uint64_t last = k == 'B' ? e : b + 1;
+      for (uint64_t j = b; j < last; ++j) {
+        put_c(' ');
+        put_u(values[j]);
+        if (k != 'D') {
+          put_c(' ');
+          put_u(priorities[j]);
+        }
+      }
+    }
+    put_c('\n');
   }
-  return out ? PBH_OK : fail(PBH_TRACE, "write failed");
+  flush();
+  ok = (std::fclose(f) == 0) && ok;
+  return ok ? PBH_OK : fail(PBH_TRACE, "write failed");
 }
 
 int pbh_trace_save_binary(const char* path, uint64_t n_ops, const uint8_t* kinds,

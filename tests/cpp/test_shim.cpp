@@ -1,6 +1,7 @@
 // Reference-style tests compiled against the C++ drop-in (include/pbh_gpu.hpp).
 // The bodies restate /root/reference/proj/tests/test_bucket_heap.cpp:87-160,
-// test_engine.cpp:31-85,156-164 and test_sssp.cpp:47-82 with only the
+// test_engine.cpp:31-85,156-164, test_sssp.cpp:47-82,180-185 and the
+// graphs.hpp accessors / validate_graph with only the
 // namespace switched: `namespace pbh = ::pbh::gpu`. Prints "ok N" on success,
 // "FAIL <where>" and exits 1 otherwise. Built and run by tests/test_cpp_shim.py.
 #include <algorithm>
@@ -150,6 +151,40 @@ int main() {
     CHECK(r3.dist[3] == pb::kInfDist);
     CHECK(r3.settled_order.size() == 3);
     CHECK_THROWS_AS(pb::par_dijkstra(make_graph(2, {{0, 1, 1}}), 2, cfg(0)), pb::PreconditionError);
+  }
+  // distance CSV and checksum (test_sssp.cpp:180-185), host-only
+  {
+    using pb::distances_to_csv;
+    using pb::distance_checksum;
+    using pb::kInfDist;
+    std::vector<std::uint64_t> dist = {0, 4, kInfDist};
+    CHECK(distances_to_csv(dist) == "vertex,dist\n0,0\n1,4\n2,inf\n");
+    CHECK(distance_checksum(dist) == distance_checksum({0, 4, kInfDist}));
+    CHECK(distance_checksum(dist) != distance_checksum({0, 5, kInfDist}));
+  }
+  // CsrGraph accessors (graphs.hpp:18-19) and validate_graph (graphs.cpp:55-72)
+  {
+    auto g = make_graph(4, {{0, 1, 1}, {0, 2, 3}, {0, 3, 1}, {2, 3, 1}});
+    CHECK(g.max_out_degree() == 3);
+    auto g2 = g;
+    CHECK(g2 == g);
+    g2.weights[1] = 4;
+    CHECK(!(g2 == g));
+    pb::validate_graph(g);
+    auto bad = g;
+    bad.targets[1] = 9;
+    CHECK_THROWS_AS(pb::validate_graph(bad), pb::InvariantError);
+    bad = g;
+    bad.weights[0] = 0;
+    CHECK_THROWS_AS(pb::validate_graph(bad), pb::InvariantError);
+    bad = g;
+    bad.offsets.pop_back();
+    CHECK_THROWS_AS(pb::validate_graph(bad), pb::InvariantError);
+    // bellman_ford agrees with par_dijkstra (test_sssp.cpp:92-100 pattern)
+    auto bf = pb::bellman_ford(g, 0);
+    auto dj = pb::par_dijkstra(g, 0, cfg(0));
+    CHECK(bf.dist == dj.dist);
+    CHECK(bf.settled_order == dj.settled_order);
   }
   std::printf("ok %d\n", g_checks);
   return 0;

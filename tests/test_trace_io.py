@@ -112,3 +112,48 @@ def test_chunked_replay_matches_oracle(pbh, tio, O, tmp_path):
     v, pr, ms = tio.run_trace_file(eng, p, chunk_ops=1500)
     assert np.array_equal(v, want_v) and np.array_equal(pr, want_p)
     assert eng.check_invariants() == []
+
+
+_TRICKY = [
+    "U 1 2\n", "U\t1\t2\r\n", "  U   7 8   \n", "B 2 1 5 4 6\n", "B 1 3 +9\n", "U +4 5\n",
+    "U 1 -1\n", "U -1 3\n", "U 1 18446744073709551615\n", "U 1 18446744073709551616\n",
+    "U 4294967295 0\n", "U 4294967296 0\n", "U 1 2x\n", "U 1x 2\n", "U 1 2 # c\n",
+    "U 1 2#c\n", "U 1# 2\n", "#only\n\n\n", "", "E\nE\n", "E x\n", "D 5\n", "D\n",
+    "D 5 6\n", "B 0\n", "B 16777217 1 1\n", "B 2 1 2\n", "B 2 1 2 3\n", "B x\n",
+    "X\n", "UU 1 2\n", "u 1 2\n", "U 1 2\nE\nD 1\nB 3 1 1 2 2 3 3\nE\n", "U 1 2", "\n\nE",
+    "U 00012 0003\n", "U 1\x0b2\n", "U 1\x0c2\n", "U - 2\n", "U + 2\n", "U 1 --2\n",
+]
+
+
+@pytest.mark.skipif(not __import__("os").path.exists(__import__("os").path.join(
+    __import__("os").path.dirname(__file__), "..", "oracle", "_ref", "libpbhref.so")),
+    reason="oracle/_ref not built")
+@pytest.mark.parametrize("i", range(len(_TRICKY)))
+def test_text_parser_matches_reference(tio, O, tmp_path, i):
+    """Our single-pass tokenizer against the reference's istream parser
+    (trace_format.cpp:34-98) on edge cases: same ops, or same op index and
+    message."""
+    from paper_1908_09378_b200 import TraceError
+    p = tmp_path / "t.txt"
+    p.write_bytes(_TRICKY[i].encode())
+    try:
+        want = O.ref_load_text(p)
+        werr = None
+    except O.RefError as e:
+        want, werr = None, e
+    try:
+        got = tio.load_text(p)
+        gerr = None
+    except TraceError as e:
+        got, gerr = None, e
+    if werr is not None:
+        assert gerr is not None, f"reference rejects {_TRICKY[i]!r}: {werr}"
+        assert gerr.op_index == werr.op_index
+        assert str(werr).split(": ", 1)[1] in str(gerr)
+    else:
+        assert gerr is None, f"reference accepts {_TRICKY[i]!r}: {gerr}"
+        assert np.array_equal(got.kinds, want.kinds)
+        assert np.array_equal(got.offsets, want.offsets)
+        assert np.array_equal(got.vals, want.vals)
+        keep = np.repeat(want.kinds, np.diff(want.offsets).astype(np.int64)) != ord("D")
+        assert np.array_equal(np.asarray(got.prios)[keep], np.asarray(want.prios)[keep])
