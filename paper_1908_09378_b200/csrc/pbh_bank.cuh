@@ -1259,7 +1259,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
       // a large batch is validated and classified by the whole grid: only
       // the elements that touch level 0 stay with this CTA (list `lst`)
       const bool big = bj != nullptr && gridDim.x > 1 && n >= kBigBatch;
-      u32 m_apply = n, stg_n = 0;
+      u32 m_apply = n, stg_n = 0, big_src = 0;
       const u32* lst = nullptr;
       if (big) {
         if (tid == 0) {
@@ -1275,23 +1275,72 @@ __global__ void __launch_bounds__(32 * NW, 1)
           bj->debug = debug ? 1u : 0u;
           bj->c0 = C0;
           bj->stg_n = bj->ll_n = bj->fresh = bj->errs = 0;
+          bj->pmin = ~0ull;
+          bj->pmax = 0;
           T.g.job.ext = bj;
         }
         __threadfence();
         Bk::sync();
-        grid_run<B>(gj, gridDim.x, 2, Run{}, Run{}, 0, Sink{}, 0, T.g, T.g.scr);
+        // one pass: every precondition checked and every element routed,
+        // nothing mutated (the index is published by the sort job below)
+        grid_run<B>(gj, gridDim.x, 6, Run{}, Run{}, 0, Sink{}, 0, T.g, T.g.scr);
         const u32 errs = *(volatile u32*)&bj->errs;
         if (errs) {
           hc.fail(errs & 1 ? PBH_ERR_UNSORTED : errs & 2 ? PBH_ERR_KEY_RANGE
                   : errs & 4 ? PBH_ERR_REINSERT : PBH_ERR_INCREASE);
           break;
         }
-        grid_run<B>(gj, gridDim.x, 3, Run{}, Run{}, 0, Sink{}, 0, T.g, T.g.scr);
         m_apply = *(volatile u32*)&bj->ll_n;
         stg_n = *(volatile u32*)&bj->stg_n;
         live += *(volatile u32*)&bj->fresh;
         lst = bj->ll;
         TPROF(6);
+        if (stg_n) {
+          // the HBM-bound part of the batch, sorted by (p, k) on the grid:
+          // a bucket sort (one job) when the buckets fit the CTA tiles,
+          // else CTA-sorted chunks + merge passes; both publish the staged
+          // elements' index entries before the leader applies its own part
+          const u32 G = gridDim.x;
+          u32 nb = G * ((stg_n + G * 1024u - 1) / (G * 1024u));
+          const bool bucketed = nb <= kBucketMax;
+          if (bucketed) {
+            const u64 pmin = *(volatile u64*)&bj->pmin, pmax = *(volatile u64*)&bj->pmax;
+            const u64 range = pmax - pmin;  // bucket q: priorities pmin + [q, q + 1) * width
+            if (range < (u64)nb - 1) nb = (u32)range + 1;
+            for (u32 i = tid; i < nb; i += B) bj->bcnt[i] = 0;
+            if (tid == 0) {
+              bj->nbkt = nb;
+              bj->bwidth = range / nb + 1;
+              bj->bovf = 0;
+            }
+            __threadfence();
+            Bk::sync();
+            grid_run<B>(gj, G, 7, Run{}, Run{}, 0, Sink{}, 0, T.g, T.g.scr);
+            big_src = 1;
+          }
+          if (!bucketed || *(volatile u32*)&bj->bovf) {
+            if (tid == 0) {
+              bj->sort_n = stg_n;
+              bj->src = bucketed ? 1u : 0u;
+              bj->write_idx = bucketed ? 0u : 1u;
+            }
+            __threadfence();
+            Bk::sync();
+            grid_run<B>(gj, G, 4, Run{}, Run{}, 0, Sink{}, 0, T.g, T.g.scr);
+            big_src = bucketed ? 1u : 0u;
+            for (u32 w = kSortChunk; w < stg_n; w <<= 1) {
+              if (tid == 0) {
+                bj->width = w;
+                bj->src = big_src;
+              }
+              __threadfence();
+              Bk::sync();
+              grid_run<B>(gj, G, 5, Run{}, Run{}, 0, Sink{}, 0, T.g, T.g.scr);
+              big_src ^= 1;
+            }
+          }
+          TPROF(8 - 1);
+        }
       }
       // pass 1: validate (no mutation)
       bool bad_sort = false, bad_key = false, bad_dead = false, bad_inc = false;
@@ -1444,29 +1493,9 @@ __global__ void __launch_bounds__(32 * NW, 1)
       if (cold_fail) break;
       TPROF(1);
       if (big && stg_n) {
-        // the HBM-bound part of the batch: grid sort (chunks, then merge
-        // passes), one push_down of the sorted run into S_1
-        if (tid == 0) {
-          bj->sort_n = stg_n;
-          bj->src = 0;
-        }
-        __threadfence();
-        Bk::sync();
-        grid_run<B>(gj, gridDim.x, 4, Run{}, Run{}, 0, Sink{}, 0, T.g, T.g.scr);
-        u32 src = 0;
-        for (u32 w = kSortChunk; w < stg_n; w <<= 1) {
-          if (tid == 0) {
-            bj->width = w;
-            bj->src = src;
-          }
-          __threadfence();
-          Bk::sync();
-          grid_run<B>(gj, gridDim.x, 5, Run{}, Run{}, 0, Sink{}, 0, T.g, T.g.scr);
-          src ^= 1;
-        }
-        TPROF(8 - 1);
+        // one push_down of the sorted staged run into S_1
         BANK_TO_H();
-        H.push_run(bj->sk[src], bj->sp[src], stg_n);
+        H.push_run(bj->sk[big_src], bj->sp[big_src], stg_n);
         BANK_FROM_H();
         if (hc.failed()) break;
         TPROF(2);

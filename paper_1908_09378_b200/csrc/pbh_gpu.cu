@@ -64,8 +64,11 @@ int current_device() {
 }
 
 // Banked op-trace interpreter (pbh_bank.cuh): 4 warps, level 0 = 1024 slots.
-constexpr int kTraceNW = 4;
-constexpr int kTraceKI = 8;
+#ifndef PBH_TRACE_NW
+#define PBH_TRACE_NW 8
+#endif
+constexpr int kTraceNW = PBH_TRACE_NW;
+constexpr int kTraceKI = 1024 / (32 * kTraceNW);  // level 0 = 1024 slots
 using TraceImage = BankL0<32 * kTraceNW, kTraceKI>;
 using TraceSmem = TraceBankSmem<kTraceNW, kTraceKI, VT>;
 
@@ -555,6 +558,18 @@ pbh_status exec_host(pbh_heap* h, u64 n_ops, const u8* kinds, const u64* off, co
   return rs;
 }
 
+// PBH_PROF builds: print and reset the leader's cycle breakdown (thread 0
+// of the interpreter CTA; categories of k_trace_bank's TPROF / BankHeap::pr).
+void prof_report(pbh_heap* h, const char* when) {
+  unsigned long long pc[16];
+  if (cudaMemcpy(pc, h->d_prof, sizeof pc, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  cudaMemset(h->d_prof, 0, sizeof pc);
+  fprintf(stderr, "pbh_prof[%s] cycles: validate %llu apply %llu bulk_cold %llu extract %llu refill %llu tail %llu pre %llu big_sort %llu"
+          " | sort %llu push_down %llu resolve1 %llu r2 %llu r3 %llu r4 %llu r5 %llu r6+ %llu\n",
+          when, pc[0], pc[1], pc[2], pc[3], pc[4], pc[5], pc[6], pc[7], pc[8], pc[9], pc[10], pc[11],
+          pc[12], pc[13], pc[14], pc[15]);
+}
+
 pbh_status single_op(pbh_heap* h, u8 kind, const u32* vals, const u64* prios, u64 n, u32* ov,
                      u64* op) {
   u64 off[2] = {0, n};
@@ -627,10 +642,15 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
     const u64 cap = std::min<u64>(d, kMaxBatch);
     BatchJob hb{};
     void* mem[6] = {};
+    void* bc = nullptr;
     const size_t sz[6] = {sizeof(BatchJob), cap * 4, cap * 8, cap * 4, cap * 8, cap * 4};
     for (int i = 0; i < 6; ++i)
       if (cudaMalloc(&mem[i], sz[i]) != cudaSuccess) return fail(set_err(PBH_OOM, "batch buffers"));
     for (int i = 0; i < 6; ++i) h->H.allocs.push_back(mem[i]);
+    if (cudaMalloc(&bc, kBucketMax * sizeof(u32)) != cudaSuccess)
+      return fail(set_err(PBH_OOM, "batch buffers"));
+    h->H.allocs.push_back(bc);
+    hb.bcnt = (u32*)bc;
     h->d_batch = (BatchJob*)mem[0];
     hb.sk[0] = (u32*)mem[1];
     hb.sp[0] = (u64*)mem[2];
@@ -660,12 +680,7 @@ pbh_status pbh_heap_destroy(pbh_heap* h) {
   cudaFree(h->d_job);
   cudaFree(h->d_save);
   if (h->d_prof) {
-    unsigned long long pc[16];
-    cudaMemcpy(pc, h->d_prof, sizeof pc, cudaMemcpyDeviceToHost);
-    fprintf(stderr, "pbh_prof cycles: validate %llu apply %llu bulk_cold %llu extract %llu refill %llu tail %llu pre %llu big_sort %llu"
-            " | sort %llu push_down %llu resolve1 %llu r2 %llu r3 %llu r4 %llu r5 %llu r6+ %llu\n",
-            pc[0], pc[1], pc[2], pc[3], pc[4], pc[5], pc[6], pc[7], pc[8], pc[9], pc[10], pc[11], pc[12],
-            pc[13], pc[14], pc[15]);
+    prof_report(h, "destroy");
     cudaFree(h->d_prof);
   }
   cudaFree(h->d_kinds);
@@ -920,6 +935,7 @@ pbh_status pbh_heap_run_trace(pbh_heap* h, uint64_t n_ops, const uint8_t* kinds,
   }
   pbh_status st = exec_host(h, n_ops, kinds, offsets, values, priorities, out_values,
                             out_priorities, n_out, failed_op, 0, wall_ms);
+  if (h->d_prof) prof_report(h, "run_trace");
   if (st == PBH_EMPTY || st == PBH_PRECONDITION) {
     return set_err(PBH_TRACE, g_last_error);  // TraceError(op_index) (engine.cpp:213-219)
   }

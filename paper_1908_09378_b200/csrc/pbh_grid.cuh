@@ -185,7 +185,8 @@ struct GridJob {
   u32 seq;   // bumped by the leader to publish a job
   u32 done;  // helpers that finished the current job
   u32 kind;  // 0 = merge, 1 = exit, 2 = validate batch, 3 = classify batch,
-             // 4 = sort chunks, 5 = merge pass (BatchJob in `ext`)
+             // 4 = sort chunks, 5 = merge pass, 6 = validate + classify (no
+             // mutation), 7 = bucket sort of the staged run (BatchJob in `ext`)
   u32 nblk;  // CTAs in the grid (leader included)
   const u32* ak;
   const u64* ap;
@@ -224,9 +225,16 @@ struct BatchJob {
   u32* sk[2];
   u64* sp[2];
   u32 sort_n, width, src;
+  u32 write_idx;  // kind 4: also publish the chunk's index entries
   // counters (atomics)
   u32 stg_n, ll_n, fresh, errs;
+  // kind 6: priority range of the staged elements; kind 7: buckets
+  u64 pmin, pmax, bwidth;
+  u32* bcnt;      // per-bucket element counts (kBucketMax)
+  u32 nbkt, bovf; // bucket count; set when a bucket exceeds kGridTile
+  u32 bar_cnt, bar_gen;  // grid barrier inside a job
 };
+constexpr u32 kBucketMax = 1184;  // 8 buckets per CTA of a 148-CTA grid
 
 template <int NT>
 struct GridSmem {
@@ -406,6 +414,15 @@ DEV void batch_sort_chunks(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
     cp_async_commit();
     cp_async_wait_all();
     Blk<NT>::sync();
+    if (X->write_idx) {
+      for (u32 i = threadIdx.x; i < m; i += NT) {
+        pbh_idx_entry ne;
+        ne.prio = g.ap[i];
+        ne.state = PBH_ST_LIVE | (PBH_LOC_DEEP << 2);
+        ne.parent = 0;
+        reinterpret_cast<ulonglong2*>(X->idx)[g.ak[i]] = *reinterpret_cast<const ulonglong2*>(&ne);
+      }
+    }
     cta_sort<NT / 32>(g.ak, g.ap, m, g.bk, g.bp);
     for (u32 i = threadIdx.x; i < m; i += NT) {
       K[c0 + i] = g.ak[i];
@@ -446,6 +463,180 @@ DEV void batch_merge_pass(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g, u32* scrat
   }
 }
 
+// Barrier over the G CTAs of a job (all co-resident: cooperative launch).
+// Sense by generation: read the generation, arrive; the last arrival resets
+// the count and publishes the next generation.
+template <int NT>
+DEV void job_barrier(BatchJob* X, u32 G) {
+  Blk<NT>::sync();
+  if (threadIdx.x == 0) {
+    const u32 gen = ld_acquire(&X->bar_gen);
+    __threadfence();
+    if (atomicAdd(&X->bar_cnt, 1u) == G - 1) {
+      X->bar_cnt = 0;
+      __threadfence();
+      st_release(&X->bar_gen, gen + 1);
+    } else {
+      u32 backoff = 16;
+      while (ld_acquire(&X->bar_gen) == gen) {
+        __nanosleep(backoff);
+        backoff = backoff < kPollMaxNs ? backoff * 2 : kPollMaxNs;
+      }
+    }
+    __threadfence();
+  }
+  Blk<NT>::sync();
+}
+
+// kind 6: validate this CTA's slice (bucket_heap.cpp:127-136 preconditions:
+// bit 0 unsorted, 1 key range, 2 dead value, 3 increase) and classify it in
+// the same pass, without mutating anything: an improving element whose
+// valid copy is in a level-0 slot, or that splitter_0 admits, is listed for
+// the leader; any other is appended to the HBM staging run (its index entry
+// is published by the sort job, once the whole batch is known to be valid).
+// The staged priorities' range feeds the bucket sort.
+template <int NT>
+DEV void batch_check_classify(BatchJob* X, u32 b, u32 G) {
+  const u32 n = X->n;
+  const u32 r0 = (u32)((u64)n * b / G), r1 = (u32)((u64)n * (b + 1) / G);
+  u32 fresh = 0, bad = 0;
+  u64 lo = ~0ull, hi = 0;
+  for (u32 j0 = r0; j0 < r1; j0 += NT) {
+    const u32 j = j0 + threadIdx.x;
+    bool to_leader = false, to_hbm = false;
+    u32 k = 0;
+    u64 p = 0;
+    if (j < r1) {
+      k = X->vals[j];
+      p = X->prios[j];
+      if (X->check && j > 0 && X->vals[j - 1] >= k) bad |= 1;
+      if (k >= X->universe) {
+        bad |= 2;
+      } else {
+        const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(X->idx + k));
+        const u32 st = (u32)e.y;
+        if (PBH_ST(st) == PBH_ST_DEAD) bad |= 4;
+        if (X->debug && PBH_ST(st) == PBH_ST_LIVE && p > e.x) bad |= 8;
+        const bool fr = PBH_ST(st) != PBH_ST_LIVE;
+        if (fr || p < e.x) {
+          const bool adm = X->spl_inf || p < X->spl_p || (p == X->spl_p && k <= X->spl_k);
+          if ((!fr && (st >> 2) < X->c0) || adm) {
+            to_leader = true;
+          } else {
+            to_hbm = true;
+            fresh += fr;
+            lo = min(lo, p);
+            hi = max(hi, p);
+          }
+        }
+      }
+    }
+    const u32 ls = warp_append(&X->ll_n, to_leader);
+    if (to_leader) X->ll[ls] = j;
+    const u32 hs = warp_append(&X->stg_n, to_hbm);
+    if (to_hbm) {
+      X->stg_k[hs] = k;
+      X->stg_p[hs] = p;
+    }
+  }
+  fresh = __reduce_add_sync(0xffffffffu, fresh);
+  bad = __reduce_or_sync(0xffffffffu, bad);
+  for (int s = 16; s; s >>= 1) {
+    lo = min(lo, (u64)__shfl_xor_sync(0xffffffffu, (unsigned long long)lo, s));
+    hi = max(hi, (u64)__shfl_xor_sync(0xffffffffu, (unsigned long long)hi, s));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (fresh) atomicAdd(&X->fresh, fresh);
+    if (bad) atomicOr(&X->errs, bad);
+    if (lo <= hi) {
+      atomicMin(reinterpret_cast<unsigned long long*>(&X->pmin), (unsigned long long)lo);
+      atomicMax(reinterpret_cast<unsigned long long*>(&X->pmax), (unsigned long long)hi);
+    }
+  }
+}
+
+// kind 7: sort the staged run (stg_n entries, sk/sp[0]) into sk/sp[1] by
+// (p, k) in one job: buckets are equal-width priority ranges (so bucket
+// order is priority order); (1) per-CTA histograms of its slice, bucket
+// bases by global atomics; (2) after a grid barrier, every CTA scans the
+// bucket totals and scatters its slice into the buckets, publishing each
+// element's index entry {p, LIVE, deep}; (3) after a second barrier, CTA b
+// sorts buckets b, b + G, ... in shared memory. A bucket above kGridTile
+// entries sets `bovf` (the leader then sorts sk/sp[1] by merge passes).
+template <int NT>
+DEV void batch_bucket_sort(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
+  using Bk = Blk<NT>;
+  const u32 n = X->stg_n, NB = X->nbkt;
+  const u64 pmin = X->pmin, width = X->bwidth;
+  const u32 r0 = (u32)((u64)n * b / G), r1 = (u32)((u64)n * (b + 1) / G);
+  u32* cnt = reinterpret_cast<u32*>(g.op);  // NB per-CTA counts, then cursors
+  u32* base = cnt + kBucketMax;              // NB bases (this CTA's offset in a bucket)
+  u32* start = base + kBucketMax;            // NB bucket starts
+  for (u32 i = threadIdx.x; i < NB; i += NT) cnt[i] = 0;
+  Bk::sync();
+  const u32* SK = X->sk[0];
+  const u64* SP = X->sp[0];
+  for (u32 j = r0 + threadIdx.x; j < r1; j += NT)
+    atomicAdd(&cnt[min(NB - 1, (u32)((SP[j] - pmin) / width))], 1u);
+  Bk::sync();
+  for (u32 i = threadIdx.x; i < NB; i += NT) {
+    const u32 c = cnt[i];
+    base[i] = c ? atomicAdd(&X->bcnt[i], c) : 0;
+    cnt[i] = 0;  // becomes the scatter cursor
+  }
+  job_barrier<NT>(X, G);
+  // bucket starts: exclusive scan of the totals (every CTA, NB <= kBucketMax)
+  {
+    u32 run = 0;
+    for (u32 i0 = 0; i0 < NB; i0 += NT) {
+      const u32 i = i0 + threadIdx.x;
+      const u32 v = i < NB ? __ldcg(&X->bcnt[i]) : 0;
+      u32 tot;
+      const u32 e = run + Bk::scan_excl(v, tot, g.scr);
+      if (i < NB) start[i] = e;
+      run += tot;
+    }
+  }
+  Bk::sync();
+  u32* DK = X->sk[1];
+  u64* DP = X->sp[1];
+  for (u32 j = r0 + threadIdx.x; j < r1; j += NT) {
+    const u32 k = SK[j];
+    const u64 p = SP[j];
+    const u32 q = min(NB - 1, (u32)((p - pmin) / width));
+    const u32 pos = start[q] + base[q] + atomicAdd(&cnt[q], 1u);
+    DK[pos] = k;
+    DP[pos] = p;
+    pbh_idx_entry ne;
+    ne.prio = p;
+    ne.state = PBH_ST_LIVE | (PBH_LOC_DEEP << 2);
+    ne.parent = 0;
+    reinterpret_cast<ulonglong2*>(X->idx)[k] = *reinterpret_cast<const ulonglong2*>(&ne);
+  }
+  job_barrier<NT>(X, G);
+  for (u32 q = b; q < NB; q += G) {
+    const u32 m = __ldcg(&X->bcnt[q]), s0 = start[q];
+    if (m > kGridTile) {
+      if (threadIdx.x == 0) atomicOr(&X->bovf, 1u);
+      continue;
+    }
+    if (m < 2) continue;
+    for (u32 i = threadIdx.x; i < m; i += NT) {
+      cp_async4(&g.ak[i], DK + s0 + i, true);
+      cp_async8(&g.ap[i], DP + s0 + i);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    Bk::sync();
+    cta_sort<NT / 32>(g.ak, g.ap, m, g.bk, g.bp);
+    for (u32 i = threadIdx.x; i < m; i += NT) {
+      DK[s0 + i] = g.ak[i];
+      DP[s0 + i] = g.ap[i];
+    }
+    Bk::sync();
+  }
+}
+
 // This CTA's share (block b of G) of the current job.
 template <int NT>
 DEV void grid_share(const GridJob& J, u32 b, GridSmem<NT>& g, u32* scratch) {
@@ -455,6 +646,8 @@ DEV void grid_share(const GridJob& J, u32 b, GridSmem<NT>& g, u32* scratch) {
     case 3: return batch_classify<NT>(J.ext, b, G);
     case 4: return batch_sort_chunks<NT>(J.ext, b, G, g);
     case 5: return batch_merge_pass<NT>(J.ext, b, G, g, scratch);
+    case 6: return batch_check_classify<NT>(J.ext, b, G);
+    case 7: return batch_bucket_sort<NT>(J.ext, b, G, g);
     default: break;
   }
   const u32 r0 = (u32)((u64)J.c * b / G), r1 = (u32)((u64)J.c * (b + 1) / G);
