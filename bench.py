@@ -455,7 +455,9 @@ def leg_c4(P, gen, dev, peak, ds, cpu):
         t.kinds = np.full(nb, ord("B"), np.uint8)
         t.offsets = np.arange(nb + 1, dtype=np.uint64) * d
         t.vals, t.prios = v, p
-        ms = eng.run_trace(t).metrics.wall_ms
+        # the batches as a caller's bulk_update loop (no closing drain), like
+        # the reference's timed Engine::bulk_update calls
+        ms = eng.run_ops(t).metrics.wall_ms
         ups = len(v) / (ms / 1e3)
         rec = {"d": d, "batches": nb, "updates": len(v), "ms": ms, "updates_per_s": ups,
                "us_per_batch": ms * 1e3 / nb, "prefill_s": pre_s,

@@ -113,6 +113,18 @@ pbh_status pbh_heap_run_trace(pbh_heap* h, uint64_t n_ops, const uint8_t* kinds,
                               const uint64_t* priorities, uint32_t* out_values,
                               uint64_t* out_priorities, uint64_t* n_out, uint64_t* failed_op,
                               double* wall_ms);
+/* The op sequence of a trace executed exactly as the same sequence of
+ * single-client calls (Engine::update / bulk_update / extract_min /
+ * delete_value, engine.cpp:90-109) would execute it, in ONE device
+ * submission, WITHOUT run_trace's closing drain: the device form of a
+ * caller's loop over bulk_update (the C4 sweep is timed through it, like the
+ * reference's bulk_update batches). Same arguments and errors as
+ * pbh_heap_run_trace (a failing op -> PBH_TRACE with *failed_op). */
+pbh_status pbh_heap_run_ops(pbh_heap* h, uint64_t n_ops, const uint8_t* kinds,
+                            const uint64_t* offsets, const uint32_t* values,
+                            const uint64_t* priorities, uint32_t* out_values,
+                            uint64_t* out_priorities, uint64_t* n_out, uint64_t* failed_op,
+                            double* wall_ms);
 /* Same with every pointer in device memory (inputs resident in HBM). */
 pbh_status pbh_heap_run_trace_device(pbh_heap* h, uint64_t n_ops, const uint8_t* d_kinds,
                                      const uint64_t* d_offsets, const uint32_t* d_values,

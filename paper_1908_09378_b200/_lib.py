@@ -44,6 +44,8 @@ SIGNATURES = {
     "pbh_heap_check_invariants": (C.c_int, [C.c_void_p, U64P]),
     "pbh_heap_run_trace": (C.c_int, [C.c_void_p, C.c_uint64, U8P, U64P, U32P, U64P, U32P, U64P,
                                      U64P, U64P, DBLP]),
+    "pbh_heap_run_ops": (C.c_int, [C.c_void_p, C.c_uint64, U8P, U64P, U32P, U64P, U32P, U64P,
+                                   U64P, U64P, DBLP]),
     "pbh_heap_run_trace_device": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, U64P,
                                             U64P, DBLP]),

@@ -43,6 +43,7 @@ namespace pbh_dev {
 
 constexpr int kBankQ = 4096;    // push-buffer capacity (entries beyond the splitter)
 constexpr int kBankPass = 256;  // edges relaxed per pass
+constexpr u32 kGridFlushMin = 1024;  // push-buffer flushes at least this large sort on the grid
 
 // The part of the shared-memory image that survives a NEED_GROW relaunch.
 template <int B, int KI, bool MW = false>
@@ -95,6 +96,8 @@ struct BankSmem {
   BankOffer ex[2][NW];  // per-pass exchange (parity double-buffered)
   LeanOffer lx[2][NW];  // the SSSP rounds' lean exchange
   u8 dirty[2][B];       // decreased-bank flags (parity double-buffered)
+  u64 fr_lo[NW], fr_hi[NW];  // grid flush: per-warp priority range
+  u32 fr_nb;
   HeapSmem<B, VT> hs;
 #ifdef PBH_XPROF
   long long xarr[2][NW];  // per-warp barrier arrival clocks (diagnostics)
@@ -374,6 +377,7 @@ struct BankHeap {
   u32 n_l0;
   u32 qn;  // push-buffer fill (mirrors L.qn at pass boundaries)
   unsigned long long* prof = nullptr;  // PBH_PROF counters 8.. (cold-path breakdown)
+  BatchJob* bj = nullptr;  // grid sort buffers (trace interpreter with helpers)
   DEV void pr(int i, long long& t) {
     if (prof && tid == 0) {
       const long long t1 = clock64();
@@ -457,15 +461,69 @@ struct BankHeap {
     const u32 n = qn;
     if (n == 0) return;
     long long t = clock64();
-    // through bank_smem() (not the member references) so the inlined sort
-    // sees the shared address space and uses LDS/STS
-    auto& SS = bank_smem<NW, KI, VT, MW>();
-    cta_sort<NW>(SS.l0.qk, SS.l0.qp, n, SS.sk, SS.sp);
-    pr(8, t);
-    push_run(L.qk, L.qp, n);
+    if (bj && hc.gj && n >= kGridFlushMin && grid_flush_sort(n)) {
+      pr(8, t);
+      push_run(bj->sk[1], bj->sp[1], n);
+    } else {
+      // through bank_smem() (not the member references) so the inlined sort
+      // sees the shared address space and uses LDS/STS
+      auto& SS = bank_smem<NW, KI, VT, MW>();
+      cta_sort<NW>(SS.l0.qk, SS.l0.qp, n, SS.sk, SS.sp);
+      pr(8, t);
+      push_run(L.qk, L.qp, n);
+    }
     if (tid == 0) L.qn = 0;
     qn = 0;
     Bk::sync();
+  }
+
+  // The push buffer sorted by the whole grid: staged to HBM (bj->sk/sp[0])
+  // with its priority range, bucket-sorted into bj->sk/sp[1] (grid job 7,
+  // index untouched). False when a bucket overflowed (the caller sorts in
+  // the CTA; the push buffer is still intact).
+  NOINL bool grid_flush_sort(u32 n) {
+    u64 lo = ~0ull, hi = 0;
+    for (u32 i = tid; i < n; i += B) {
+      const u64 p = L.qp[i];
+      bj->sk[0][i] = L.qk[i];
+      bj->sp[0][i] = p;
+      lo = min(lo, p);
+      hi = max(hi, p);
+    }
+    for (int s = 16; s; s >>= 1) {
+      lo = min(lo, (u64)__shfl_xor_sync(0xffffffffu, (unsigned long long)lo, s));
+      hi = max(hi, (u64)__shfl_xor_sync(0xffffffffu, (unsigned long long)hi, s));
+    }
+    if ((tid & 31) == 0) {
+      S.fr_lo[tid >> 5] = lo;
+      S.fr_hi[tid >> 5] = hi;
+    }
+    Bk::sync();
+    const u32 G = hc.gsz;
+    if (tid == 0) {
+      u64 a = ~0ull, b = 0;
+      for (int w = 0; w < NW; ++w) {
+        a = min(a, S.fr_lo[w]);
+        b = max(b, S.fr_hi[w]);
+      }
+      const u64 range = b - a;
+      u32 nb = G;
+      if (range < (u64)nb - 1) nb = (u32)range + 1;
+      bj->stg_n = n;
+      bj->pmin = a;
+      bj->pmax = b;
+      bj->nbkt = nb;
+      bj->bwidth = range / nb + 1;
+      bj->bovf = 0;
+      bj->write_idx = 0;
+      S.fr_nb = nb;
+    }
+    Bk::sync();
+    for (u32 i = tid; i < S.fr_nb; i += B) bj->bcnt[i] = 0;
+    __threadfence();
+    Bk::sync();
+    grid_run<B>(hc.gj, G, 7, Run{}, Run{}, 0, Sink{}, 0, *hc.gs, hc.gs->scr);
+    return *(volatile u32*)&bj->bovf == 0;
   }
 
   // Rebuild level 0 from the sorted run (K, P)[0, n), n <= C0: entry j goes
@@ -1138,6 +1196,10 @@ __global__ void __launch_bounds__(32 * NW, 1)
   BankL0<B, KI>& L = S.l0;
   BH H(hc, S, g->idx, nullptr);
   H.prof = prof;
+  if (gridDim.x > 1 && bj) {
+    H.bj = bj;
+    if (tid == 0) T.g.job.ext = bj;
+  }
   pbh_idx_entry* const idx = g->idx;
   const u64 universe = g->universe;
   // batches beyond the large-batch buffers (2^26 entries) are rejected, not split
@@ -1312,6 +1374,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
               bj->nbkt = nb;
               bj->bwidth = range / nb + 1;
               bj->bovf = 0;
+              bj->write_idx = 1;
             }
             __threadfence();
             Bk::sync();
@@ -1340,6 +1403,16 @@ __global__ void __launch_bounds__(32 * NW, 1)
             }
           }
           TPROF(8 - 1);
+          // one push_down of the sorted staged run into S_1, before the
+          // leader's own part: the push-buffer flushes of that part reuse
+          // the grid sort buffers (the order of pushes into S_1 does not
+          // matter: it is a set, and the staged elements lie beyond
+          // splitter_0, which the leader's part can only lower)
+          BANK_TO_H();
+          H.push_run(bj->sk[big_src], bj->sp[big_src], stg_n);
+          BANK_FROM_H();
+          if (hc.failed()) break;
+          TPROF(2);
         }
       }
       // pass 1: validate (no mutation)
@@ -1492,14 +1565,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
       }
       if (cold_fail) break;
       TPROF(1);
-      if (big && stg_n) {
-        // one push_down of the sorted staged run into S_1
-        BANK_TO_H();
-        H.push_run(bj->sk[big_src], bj->sp[big_src], stg_n);
-        BANK_FROM_H();
-        if (hc.failed()) break;
-        TPROF(2);
-      }
+
       if (tid == 0) sm.touches[0] += 2ull * n;
     } else if (kind == 'E' || (kind == kOpFind && allow_internal)) {
       // ------------------------------------------------ extract_min / find_min

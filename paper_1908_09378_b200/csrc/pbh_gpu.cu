@@ -416,7 +416,7 @@ struct pbh_heap {
   TraceImage* d_save = nullptr; // its level-0 image between launches
   u32 grid_min = kGridMin;
   unsigned long long* d_prof = nullptr;  // PBH_PROF: leader cycle breakdown
-  BatchJob* d_batch = nullptr;           // large-batch grid job (d >= kBigBatch)
+  BatchJob* d_batch = nullptr;           // grid sort job (large batches, push-buffer flushes)
   // staging for host traces
   u64 st_ops = 0, st_el = 0, st_out = 0;
   u8* d_kinds = nullptr;
@@ -637,9 +637,10 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
     if (e != cudaSuccess) return fail(set_err(PBH_CUDA, "level-0 image init failed"));
   }
   if (const char* e = getenv("PBH_GRID_MIN")) h->grid_min = std::max(2, atoi(e));
-  if (h->d_job && d >= kBigBatch) {
-    // large batches: job block + staging / sort ping-pong / leader list
-    const u64 cap = std::min<u64>(d, kMaxBatch);
+  if (h->d_job) {
+    // grid sorts: job block + staging / sort ping-pong / leader list, for
+    // large batches (d >= kBigBatch) and the push-buffer flushes (kBankQ)
+    const u64 cap = std::max<u64>(std::min<u64>(d, kMaxBatch), kBankQ);
     BatchJob hb{};
     void* mem[6] = {};
     void* bc = nullptr;
@@ -907,11 +908,13 @@ pbh_status pbh_heap_check_invariants(pbh_heap* h, uint64_t* n_violations) {
   return PBH_OK;
 }
 
-pbh_status pbh_heap_run_trace(pbh_heap* h, uint64_t n_ops, const uint8_t* kinds,
-                              const uint64_t* offsets, const uint32_t* values,
-                              const uint64_t* priorities, uint32_t* out_values,
-                              uint64_t* out_priorities, uint64_t* n_out, uint64_t* failed_op,
-                              double* wall_ms) {
+namespace {
+// run_trace (drain = true) and run_ops (drain = false) over host arrays.
+pbh_status run_host_ops(pbh_heap* h, uint64_t n_ops, const uint8_t* kinds,
+                        const uint64_t* offsets, const uint32_t* values,
+                        const uint64_t* priorities, uint32_t* out_values,
+                        uint64_t* out_priorities, uint64_t* n_out, uint64_t* failed_op,
+                        double* wall_ms, bool drain) {
   if (!h) return set_err(PBH_PRECONDITION, "null heap");
   if (failed_op) *failed_op = ~0ull;
   if (n_out) *n_out = 0;
@@ -935,11 +938,11 @@ pbh_status pbh_heap_run_trace(pbh_heap* h, uint64_t n_ops, const uint8_t* kinds,
   }
   pbh_status st = exec_host(h, n_ops, kinds, offsets, values, priorities, out_values,
                             out_priorities, n_out, failed_op, 0, wall_ms);
-  if (h->d_prof) prof_report(h, "run_trace");
+  if (h->d_prof) prof_report(h, drain ? "run_trace" : "run_ops");
   if (st == PBH_EMPTY || st == PBH_PRECONDITION) {
     return set_err(PBH_TRACE, g_last_error);  // TraceError(op_index) (engine.cpp:213-219)
   }
-  if (st) return st;
+  if (st || !drain) return st;
   // Engine::run_trace drains before returning (engine.cpp:221)
   double dms = 0;
   u8 k = kOpDrain;
@@ -947,6 +950,25 @@ pbh_status pbh_heap_run_trace(pbh_heap* h, uint64_t n_ops, const uint8_t* kinds,
   st = exec_host(h, 1, &k, off, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 1, &dms);
   if (wall_ms) *wall_ms += dms;
   return st;
+}
+}  // namespace
+
+pbh_status pbh_heap_run_trace(pbh_heap* h, uint64_t n_ops, const uint8_t* kinds,
+                              const uint64_t* offsets, const uint32_t* values,
+                              const uint64_t* priorities, uint32_t* out_values,
+                              uint64_t* out_priorities, uint64_t* n_out, uint64_t* failed_op,
+                              double* wall_ms) {
+  return run_host_ops(h, n_ops, kinds, offsets, values, priorities, out_values, out_priorities,
+                      n_out, failed_op, wall_ms, true);
+}
+
+pbh_status pbh_heap_run_ops(pbh_heap* h, uint64_t n_ops, const uint8_t* kinds,
+                            const uint64_t* offsets, const uint32_t* values,
+                            const uint64_t* priorities, uint32_t* out_values,
+                            uint64_t* out_priorities, uint64_t* n_out, uint64_t* failed_op,
+                            double* wall_ms) {
+  return run_host_ops(h, n_ops, kinds, offsets, values, priorities, out_values, out_priorities,
+                      n_out, failed_op, wall_ms, false);
 }
 
 pbh_status pbh_heap_run_trace_device(pbh_heap* h, uint64_t n_ops, const uint8_t* d_kinds,

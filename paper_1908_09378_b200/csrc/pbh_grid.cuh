@@ -560,7 +560,8 @@ DEV void batch_check_classify(BatchJob* X, u32 b, u32 G) {
 // order is priority order); (1) per-CTA histograms of its slice, bucket
 // bases by global atomics; (2) after a grid barrier, every CTA scans the
 // bucket totals and scatters its slice into the buckets, publishing each
-// element's index entry {p, LIVE, deep}; (3) after a second barrier, CTA b
+// element's index entry {p, LIVE, deep} when write_idx (a staged batch; a
+// push-buffer flush keeps the index as it is); (3) after a second barrier, CTA b
 // sorts buckets b, b + G, ... in shared memory. A bucket above kGridTile
 // entries sets `bovf` (the leader then sorts sk/sp[1] by merge passes).
 template <int NT>
@@ -607,11 +608,13 @@ DEV void batch_bucket_sort(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
     const u32 pos = start[q] + base[q] + atomicAdd(&cnt[q], 1u);
     DK[pos] = k;
     DP[pos] = p;
-    pbh_idx_entry ne;
-    ne.prio = p;
-    ne.state = PBH_ST_LIVE | (PBH_LOC_DEEP << 2);
-    ne.parent = 0;
-    reinterpret_cast<ulonglong2*>(X->idx)[k] = *reinterpret_cast<const ulonglong2*>(&ne);
+    if (X->write_idx) {
+      pbh_idx_entry ne;
+      ne.prio = p;
+      ne.state = PBH_ST_LIVE | (PBH_LOC_DEEP << 2);
+      ne.parent = 0;
+      reinterpret_cast<ulonglong2*>(X->idx)[k] = *reinterpret_cast<const ulonglong2*>(&ne);
+    }
   }
   job_barrier<NT>(X, G);
   for (u32 q = b; q < NB; q += G) {

@@ -159,6 +159,15 @@ class Engine:
         """Engine::run_trace (engine.cpp:207-226): the whole trace in one
         device submission, then drain. ``trace`` is any object with flat
         ``kinds``/``offsets``/``vals``/``prios`` arrays."""
+        return self._run(trace, _lib.lib().pbh_heap_run_trace)
+
+    def run_ops(self, trace) -> RunResult:
+        """The trace's ops as the equivalent sequence of single-client calls
+        (update / bulk_update / extract_min / delete_value) in one device
+        submission, without run_trace's closing drain (pbh_heap_run_ops)."""
+        return self._run(trace, _lib.lib().pbh_heap_run_ops)
+
+    def _run(self, trace, fn) -> RunResult:
         kinds = np.ascontiguousarray(trace.kinds, dtype=np.uint8)
         offs = np.ascontiguousarray(trace.offsets, dtype=np.uint64)
         vals = np.ascontiguousarray(trace.vals, dtype=np.uint32)
@@ -174,10 +183,9 @@ class Engine:
             prios = np.zeros(1, np.uint64)
         if n_ops == 0:
             kinds = np.zeros(1, np.uint8)
-        st = _lib.lib().pbh_heap_run_trace(self._h, n_ops, _ptr(kinds, _lib.U8P), _ptr(offs, U64P),
-                                           _ptr(vals, U32P), _ptr(prios, U64P), _ptr(ov, U32P),
-                                           _ptr(op, U64P), C.byref(n_out), C.byref(failed),
-                                           C.byref(wall))
+        st = fn(self._h, n_ops, _ptr(kinds, _lib.U8P), _ptr(offs, U64P), _ptr(vals, U32P),
+                _ptr(prios, U64P), _ptr(ov, U32P), _ptr(op, U64P), C.byref(n_out),
+                C.byref(failed), C.byref(wall))
         raise_for(st, op_index=failed.value)
         m = self.snapshot_metrics()
         m.wall_ms = wall.value

@@ -258,3 +258,23 @@ def test_golden_trace_fixtures(pbh):
         got = engine(pbh, d).run_trace(t)
         assert np.array_equal(got.extracted_values, z[name + "_out_v"]), name
         assert np.array_equal(got.extracted_priorities, z[name + "_out_p"]), name
+
+
+@pytest.mark.parametrize("d", [1, 8, 64])
+def test_run_ops_matches_run_trace(pbh, O, d):
+    # run_ops = the same single-client calls without the closing drain: the
+    # extraction sequence is the oracle's, and a later drain + extraction of
+    # everything left agrees with run_trace's final state
+    tr = O.gen_legal_trace(4000, d, 31 + d)
+    want_v, want_p = O.run_oracle(tr)
+    eng = pbh.Engine(pbh.EngineConfig(d=d))
+    try:
+        got = eng.run_ops(tr)
+        assert np.array_equal(got.extracted_values, want_v)
+        assert np.array_equal(got.extracted_priorities, want_p)
+        n_left = eng.live_size()
+        eng.drain()
+        assert eng.check_invariants() == []
+        assert eng.live_size() == n_left
+    finally:
+        eng.close()

@@ -34,7 +34,7 @@ def c4(log2n, d, batches):
     t.kinds = np.full(nb, ord("B"), np.uint8)
     t.offsets = np.arange(nb + 1, dtype=np.uint64) * d
     t.vals, t.prios = v, p
-    m = eng.run_trace(t).metrics
+    m = eng.run_ops(t).metrics
     print(json.dumps({"cfg": "C4", "log2n": log2n, "d": d, "batches": nb, "prefill_ms": pre,
                       "ms": m.wall_ms, "us_per_batch": m.wall_ms * 1e3 / nb,
                       "updates_per_s": nb * d / (m.wall_ms / 1e3),
