@@ -93,6 +93,12 @@ pbh_status pbh_heap_drain(pbh_heap* h);
 pbh_status pbh_heap_metrics(pbh_heap* h, uint64_t* ops, uint64_t* resolves_per_level,
                             uint64_t* touches_per_level, uint32_t* n_levels);
 
+/* Storage counters (no reference counterpart): entries stored below level 0
+ * (live copies plus stale ones not yet dropped) and the stale entries the
+ * filtered grid / streamed merges have dropped so far (drop_stale_duplicates,
+ * primitives.cpp:103-120, done through the position index). */
+pbh_status pbh_heap_stats(pbh_heap* h, uint64_t* stored_deep, uint64_t* stale_dropped);
+
 /* Structural audit (BucketHeap::check_invariants, bucket_heap.cpp:302-409)
  * restated for the (priority, value)-sorted SoA levels: sortedness, splitter
  * separation, capacity, live count. Returns the number of violations in

@@ -41,6 +41,7 @@ SIGNATURES = {
     "pbh_heap_live_size": (C.c_int, [C.c_void_p, I64P]),
     "pbh_heap_drain": (C.c_int, [C.c_void_p]),
     "pbh_heap_metrics": (C.c_int, [C.c_void_p, U64P, U64P, U64P, U32P]),
+    "pbh_heap_stats": (C.c_int, [C.c_void_p, U64P, U64P]),
     "pbh_heap_check_invariants": (C.c_int, [C.c_void_p, U64P]),
     "pbh_heap_run_trace": (C.c_int, [C.c_void_p, C.c_uint64, U8P, U64P, U32P, U64P, U32P, U64P,
                                      U64P, U64P, DBLP]),

@@ -483,10 +483,12 @@ struct BankHeap {
   // the CTA; the push buffer is still intact).
   NOINL bool grid_flush_sort(u32 n) {
     u64 lo = ~0ull, hi = 0;
+    u32* const dk = bj->sk[0];
+    u64* const dp = bj->sp[0];
     for (u32 i = tid; i < n; i += B) {
       const u64 p = L.qp[i];
-      bj->sk[0][i] = L.qk[i];
-      bj->sp[0][i] = p;
+      dk[i] = L.qk[i];
+      dp[i] = p;
       lo = min(lo, p);
       hi = max(hi, p);
     }
@@ -1186,6 +1188,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
   hc.rm = g->g_rm;
   hc.bo = nullptr;
   hc.gs = &T.g;  // streamed CTA-local merges
+  grid_smem_init<B>(T.g);
   if (gridDim.x > 1) {
     hc.gj = gj;
     hc.gsz = gridDim.x;
@@ -1196,10 +1199,15 @@ __global__ void __launch_bounds__(32 * NW, 1)
   BankL0<B, KI>& L = S.l0;
   BH H(hc, S, g->idx, nullptr);
   H.prof = prof;
+  if (tid == 0) {
+    T.g.job.ext = nullptr;
+    T.g.job.idx = g->idx;
+  }
   if (gridDim.x > 1 && bj) {
     H.bj = bj;
     if (tid == 0) T.g.job.ext = bj;
   }
+  Bk::sync();
   pbh_idx_entry* const idx = g->idx;
   const u64 universe = g->universe;
   // batches beyond the large-batch buffers (2^26 entries) are rejected, not split

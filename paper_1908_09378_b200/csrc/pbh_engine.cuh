@@ -209,6 +209,115 @@ DEV u32 merge_split(const Run& A, const Run& B, u32 c, u32* scratch) {
       scratch);
 }
 
+// Both merge-path splits of one output range [c0, c1) at once: each half
+// of the CTA runs a k-ary search with NT/2 probes per round, so the two
+// HBM-latency-bound searches overlap instead of running back to back.
+// scratch: u32[NT/32 + 2].
+template <int NT>
+DEV u32 merge_split(const Run& A, const Run& B, u32 c, u32* scratch);
+
+template <int NT>
+DEV void merge_split2(const Run& A, const Run& B, u32 c0, u32 c1, u32* scratch, u32& a0, u32& a1) {
+  if constexpr (NT < 64) {  // one warp: the two searches in sequence
+    a0 = merge_split<NT>(A, B, c0, scratch);
+    a1 = merge_split<NT>(A, B, c1, scratch);
+    return;
+  } else {
+  constexpr u32 H = NT / 2;
+  const u32 half = threadIdx.x >= H, t = threadIdx.x - half * H;
+  const u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const u32 c = half ? c1 : c0;
+  u32 lo = c > B.n ? c - B.n : 0, hi = c < A.n ? c : A.n;
+  auto pred = [&](u32 a) { return less_pk(A.p[a], A.k[a], B.p[c - 1 - a], B.k[c - 1 - a]); };
+  for (;;) {
+    const bool active = lo < hi;
+    if (!__syncthreads_or(active)) break;
+    const u32 span = hi - lo;
+    bool pt = false;
+    if (active) {
+      if (span <= H) {
+        pt = t < span && pred(lo + t);
+      } else {
+        pt = pred(lo + (u32)(((u64)span * (t + 1)) / (H + 1)));
+      }
+    }
+    const u32 cnt = __popc(__ballot_sync(0xffffffffu, pt));
+    if (lane == 0) scratch[w] = cnt;
+    __syncthreads();
+    u32 ntrue = 0;
+#pragma unroll
+    for (u32 i = 0; i < H / 32; ++i) ntrue += scratch[half * (H / 32) + i];
+    __syncthreads();
+    if (active) {
+      if (span <= H) {
+        lo += ntrue;
+        hi = lo;
+      } else {
+        const u32 nl = ntrue ? lo + (u32)(((u64)span * ntrue) / (H + 1)) + 1 : lo;
+        const u32 nh = ntrue < H ? lo + (u32)(((u64)span * (ntrue + 1)) / (H + 1)) : hi;
+        lo = nl;
+        hi = nh;
+      }
+    }
+  }
+  if (t == 0) scratch[half] = lo;
+  __syncthreads();
+  a0 = scratch[0];
+  a1 = scratch[1];
+  __syncthreads();
+  }
+}
+
+// ---- 1-D TMA (cp.async.bulk) staging with an mbarrier --------------------
+DEV u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+DEV void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// Arm the barrier for `bytes` of async-proxy transfers (one arrival).
+DEV void mbar_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+DEV void mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Order this thread's earlier generic-proxy shared-memory accesses before
+// later async-proxy (TMA) writes to the same buffers.
+DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// Bulk copy of `bytes` (multiple of 16, both addresses 16-byte aligned)
+// from global memory into this CTA's shared memory, completing on `bar`.
+DEV void tma_load_1d(void* dst, const void* src, u32 bytes, u64* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// A 16-byte aligned window covering elements [i, i + n) of an array of
+// E-byte elements: source address, element offset of i inside the window,
+// and the copy size.
+template <int E>
+struct Window {
+  const void* src;
+  u32 off, bytes;
+  DEV Window(const void* base, u32 i, u32 n) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(base) + (uintptr_t)i * E;
+    const uintptr_t a0 = a & ~uintptr_t(15);
+    src = reinterpret_cast<const void*>(a0);
+    off = (u32)((a - a0) / E);
+    bytes = (u32)(((a - a0) + (uintptr_t)n * E + 15) & ~uintptr_t(15));
+  }
+};
+
 // Shared-memory scratch needed by the merge machinery.
 template <int NT, int VT>
 struct TileSmem {

@@ -45,6 +45,7 @@ pbh_status set_err(pbh_status s, const std::string& msg) {
 
 constexpr int VT = 4;
 constexpr u32 kOorCap = 4096;  // remembered out-of-index deletes per heap
+constexpr size_t kTmaSlack = 64;  // bytes past each merge buffer (TMA window over-read)
 
 u64 pow2_at_least(u64 x) {
   u64 p = 1;
@@ -96,6 +97,10 @@ cudaError_t launch_trace_bank(cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr
   if (gj && G > 1) {
     err = cudaMemsetAsync(gj, 0, sizeof(GridJob), st);
     if (err != cudaSuccess) return err;
+    if (bj) {  // the job-barrier counter restarts with every launch
+      err = cudaMemsetAsync(&bj->bar_cnt, 0, sizeof(u32), st);
+      if (err != cudaSuccess) return err;
+    }
     void* args[] = {&g, &tr, &b, &e, &ov, &op, &ks, &save, &internal, &gj, &grid_min, &prof, &bj};
     err = cudaLaunchCooperativeKernel((const void*)fn, dim3(G), dim3(32 * kTraceNW), args, smem, st);
   } else {
@@ -250,7 +255,10 @@ struct DevHeap {
   size_t measured = 0;
   static size_t a256(size_t b) { return (std::max<size_t>(b, 16) + 255) & ~size_t(255); }
 
+  // Every buffer gets kTmaSlack bytes past its end: 16-byte-aligned TMA
+  // windows over a run ending at the buffer end read up to 15 bytes beyond.
   pbh_status alloc(void** p, size_t bytes) {
+    bytes += kTmaSlack;
     const size_t b = a256(bytes);
     if (measure) {
       measured += b;
@@ -564,6 +572,18 @@ void prof_report(pbh_heap* h, const char* when) {
   unsigned long long pc[16];
   if (cudaMemcpy(pc, h->d_prof, sizeof pc, cudaMemcpyDeviceToHost) != cudaSuccess) return;
   cudaMemset(h->d_prof, 0, sizeof pc);
+  unsigned long long jp[16][2];
+  if (cudaMemcpyFromSymbol(jp, g_jobprof, sizeof jp) == cudaSuccess) {
+    static const char* names[16] = {"merge", "exit", "validate", "classify", "chunks", "pass",
+                                    "check+classify", "bucket_sort", "b:hist", "b:bar1", "b:scatter",
+                                    "b:bar2", "b:sort", "leader_wait", "filtered_merge", "-"};
+    fprintf(stderr, "pbh_jobprof[%s]:", when);
+    for (int i = 0; i < 15; ++i)
+      if (jp[i][1]) fprintf(stderr, " %s %llu x %.0f", names[i], jp[i][1], (double)jp[i][0] / jp[i][1]);
+    fprintf(stderr, "\n");
+    std::memset(jp, 0, sizeof jp);
+    cudaMemcpyToSymbol(g_jobprof, jp, sizeof jp);
+  }
   fprintf(stderr, "pbh_prof[%s] cycles: validate %llu apply %llu bulk_cold %llu extract %llu refill %llu tail %llu pre %llu big_sort %llu"
           " | sort %llu push_down %llu resolve1 %llu r2 %llu r3 %llu r4 %llu r5 %llu r6+ %llu\n",
           when, pc[0], pc[1], pc[2], pc[3], pc[4], pc[5], pc[6], pc[7], pc[8], pc[9], pc[10], pc[11],
@@ -644,7 +664,8 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
     BatchJob hb{};
     void* mem[6] = {};
     void* bc = nullptr;
-    const size_t sz[6] = {sizeof(BatchJob), cap * 4, cap * 8, cap * 4, cap * 8, cap * 4};
+    const size_t sz[6] = {sizeof(BatchJob), cap * 4 + kTmaSlack, cap * 8 + kTmaSlack,
+                          cap * 4 + kTmaSlack, cap * 8 + kTmaSlack, cap * 4};
     for (int i = 0; i < 6; ++i)
       if (cudaMalloc(&mem[i], sz[i]) != cudaSuccess) return fail(set_err(PBH_OOM, "batch buffers"));
     for (int i = 0; i < 6; ++i) h->H.allocs.push_back(mem[i]);
@@ -663,8 +684,11 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
     if (cudaMemcpy(h->d_batch, &hb, sizeof hb, cudaMemcpyHostToDevice) != cudaSuccess)
       return fail(set_err(PBH_CUDA, "batch job init"));
   }
-  if (getenv("PBH_PROF") && cudaMalloc(&h->d_prof, 16 * sizeof(unsigned long long)) == cudaSuccess)
+  if (getenv("PBH_PROF") && cudaMalloc(&h->d_prof, 16 * sizeof(unsigned long long)) == cudaSuccess) {
     cudaMemset(h->d_prof, 0, 16 * sizeof(unsigned long long));
+    const unsigned int on = 1;
+    cudaMemcpyToSymbol(g_jobprof_on, &on, sizeof on);
+  }
   cudaEventCreate(&h->ev0);
   cudaEventCreate(&h->ev1);
   *out = h;
@@ -783,6 +807,19 @@ pbh_status pbh_heap_metrics(pbh_heap* h, uint64_t* ops, uint64_t* resolves, uint
     if (touches) touches[i] = i < used ? hd.touches[i] : 0;
   }
   if (n_levels) *n_levels = used;
+  return PBH_OK;
+}
+
+pbh_status pbh_heap_stats(pbh_heap* h, uint64_t* stored_deep, uint64_t* stale_dropped) {
+  if (!h) return set_err(PBH_PRECONDITION, "null heap");
+  cudaSetDevice(h->device);
+  pbh_heap_dev hd;
+  CK(cudaMemcpyAsync(&hd, h->H.dev, sizeof(hd), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  u64 st = 0;
+  for (u32 i = 1; i < hd.n_levels; ++i) st += (u64)hd.st[i].b_size + hd.st[i].s_size;
+  if (stored_deep) *stored_deep = st;
+  if (stale_dropped) *stale_dropped = hd.stale_dropped;
   return PBH_OK;
 }
 

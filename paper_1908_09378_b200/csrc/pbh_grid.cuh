@@ -186,7 +186,8 @@ struct GridJob {
   u32 done;  // helpers that finished the current job
   u32 kind;  // 0 = merge, 1 = exit, 2 = validate batch, 3 = classify batch,
              // 4 = sort chunks, 5 = merge pass, 6 = validate + classify (no
-             // mutation), 7 = bucket sort of the staged run (BatchJob in `ext`)
+             // mutation), 7 = bucket sort of the staged run (BatchJob in `ext`),
+             // 8 = merge dropping stale entries (compacting; count in ext)
   u32 nblk;  // CTAs in the grid (leader included)
   const u32* ak;
   const u64* ap;
@@ -197,6 +198,8 @@ struct GridJob {
   u32 out_base;
   Sink sink;
   BatchJob* ext;
+  const pbh_idx_entry* idx;  // stale filter (kind 8, filtered streams): valid iff LIVE at this priority
+  u32 filter, pad_;
 };
 
 // A large bulk_update batch handled by the whole grid (kinds 2-5). The leader
@@ -232,20 +235,43 @@ struct BatchJob {
   u64 pmin, pmax, bwidth;
   u32* bcnt;      // per-bucket element counts (kBucketMax)
   u32 nbkt, bovf; // bucket count; set when a bucket exceeds kGridTile
-  u32 bar_cnt, bar_gen;  // grid barrier inside a job
+  u32 bar_cnt;    // job-barrier arrivals of the current launch (host-zeroed)
+  u32 merge_total;  // kind 8: entries written
 };
 constexpr u32 kBucketMax = 1184;  // 8 buckets per CTA of a 148-CTA grid
+constexpr u32 kRankSortMax = 192;  // buckets up to this size: rank sort (measured vs cta_sort)
 
 template <int NT>
 struct GridSmem {
   GridJob sub;  // one piece of a merge pass
-  u32 ak[kGridTile], bk[kGridTile], ok[kGridTile];
-  u64 ap[kGridTile], bp[kGridTile], op[kGridTile];
+  // merge windows (TMA destinations: 16-byte aligned, room for the
+  // alignment offset of a window start) and the output tile
+  alignas(16) u32 ak[kGridTile + 4];
+  alignas(16) u32 bk[kGridTile + 4];
+  alignas(16) u32 ok[kGridTile];
+  alignas(16) u64 ap[kGridTile + 2];
+  alignas(16) u64 bp[kGridTile + 2];
+  alignas(16) u64 op[kGridTile];
   GridJob job;  // the current job, copied in by thread 0
+  u64 mbar;     // window-load barrier (one phase per tile)
+  u32 mph;      // its next phase parity
   u32 ta;       // A elements consumed by the current tile
   u32 seq;
+  u32 bar_epoch;  // job barriers passed by this CTA in this launch
   u32 scr[NT / 32 + 2];  // scan scratch of the merge-path searches
 };
+
+// Once per CTA per launch, before any grid job or streamed merge.
+template <int NT>
+DEV void grid_smem_init(GridSmem<NT>& g) {
+  if (threadIdx.x == 0) {
+    g.seq = 0;
+    g.mph = 0;
+    g.bar_epoch = 0;
+    mbar_init(&g.mbar, 1);
+  }
+  __syncthreads();
+}
 
 DEV u32 ld_acquire(const u32* p) {
   u32 v;
@@ -256,65 +282,128 @@ DEV void st_release(u32* p, u32 v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// PBH_PROF diagnostics of the grid jobs (leader CTA, thread 0): cycles and
+// count per job kind [0, 8), and per phase of the bucket sort [8, 12).
+__device__ unsigned long long g_jobprof[16][2];
+__device__ unsigned int g_jobprof_on;
+DEV void jobprof_add(u32 slot, long long cycles) {
+  if (g_jobprof_on && threadIdx.x == 0 && blockIdx.x == 0) {
+    g_jobprof[slot][0] += (unsigned long long)cycles;
+    g_jobprof[slot][1] += 1;
+  }
+}
+
 // Stream the merge of A[ia, ia_end) and B[ib, ib_end) (no filter) into
-// sink[out ...). Every thread of the CTA calls this.
+// sink[out ...). Every thread of the CTA calls this. Per tile of kGridTile
+// outputs: the four input windows arrive by 1-D TMA bulk copies (16-byte
+// aligned windows, one mbarrier), each thread merges its merge-path slice
+// from shared memory into the output tile, and the tile is stored
+// coalesced.
 template <int NT>
-DEV void grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u32 out,
-                     GridSmem<NT>& g) {
+DEV u32 grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u32 out,
+                    GridSmem<NT>& g) {
   using Bk = Blk<NT>;
   constexpr u32 VT = kGridTile / NT;
   const u32 tid = threadIdx.x;
+  const bool filter = J.filter != 0;
+  u32 ph = g.mph;
+  u32 written = 0;
   while (ia < ia_end || ib < ib_end) {
     const u32 na = min(kGridTile, ia_end - ia), nb = min(kGridTile, ib_end - ib);
     const u32 n = min(kGridTile, (ia_end - ia) + (ib_end - ib));
-    // windows straight into shared memory (cp.async: no register round trip,
-    // every load of the tile in flight at once)
-    for (u32 i = tid; i < na; i += NT) {
-      cp_async4(&g.ak[i], J.ak + ia + i, true);
-      cp_async8(&g.ap[i], J.ap + ia + i);
+    const Window<4> wak(J.ak, ia, na), wbk(J.bk, ib, nb);
+    const Window<8> wap(J.ap, ia, na), wbp(J.bp, ib, nb);
+    if (tid == 0) {
+      fence_proxy_async_smem();  // the windows' previous readers are done (barrier above)
+      mbar_expect_tx(&g.mbar, (na ? wak.bytes + wap.bytes : 0u) + (nb ? wbk.bytes + wbp.bytes : 0u));
+      if (na) {
+        tma_load_1d(g.ak, wak.src, wak.bytes, &g.mbar);
+        tma_load_1d(g.ap, wap.src, wap.bytes, &g.mbar);
+      }
+      if (nb) {
+        tma_load_1d(g.bk, wbk.src, wbk.bytes, &g.mbar);
+        tma_load_1d(g.bp, wbp.src, wbp.bytes, &g.mbar);
+      }
     }
-    for (u32 i = tid; i < nb; i += NT) {
-      cp_async4(&g.bk[i], J.bk + ib + i, true);
-      cp_async8(&g.bp[i], J.bp + ib + i);
-    }
-    cp_async_commit();
-    cp_async_wait_all();
-    Bk::sync();
+    mbar_wait(&g.mbar, ph);
+    ph ^= 1u;
+    const u32* AK = g.ak + wak.off;
+    const u64* AP = g.ap + wap.off;
+    const u32* BK = g.bk + wbk.off;
+    const u64* BP = g.bp + wbp.off;
     // this thread's outputs [d0, d1): merge-path split inside the windows
     const u32 d0 = min(tid * VT, n), d1 = min(d0 + VT, n);
     u32 lo = d0 > nb ? d0 - nb : 0, hi = min(d0, na);
     while (lo < hi) {
       const u32 m = (lo + hi) >> 1;
-      if (less_pk(g.ap[m], g.ak[m], g.bp[d0 - 1 - m], g.bk[d0 - 1 - m]))
+      if (less_pk(AP[m], AK[m], BP[d0 - 1 - m], BK[d0 - 1 - m]))
         lo = m + 1;
       else
         hi = m;
     }
     u32 x = lo, y = d0 - lo;
+    u32 rk[VT];
+    u64 rp[VT];
 #pragma unroll
     for (u32 v = 0; v < VT; ++v) {
+      rk[v] = 0xffffffffu;
+      rp[v] = ~0ull;
       if (d0 + v < d1) {
-        const bool takeA = x < na && (y >= nb || less_pk(g.ap[x], g.ak[x], g.bp[y], g.bk[y]));
-        if (takeA) {
-          g.ok[d0 + v] = g.ak[x];
-          g.op[d0 + v] = g.ap[x];
-          ++x;
-        } else {
-          g.ok[d0 + v] = g.bk[y];
-          g.op[d0 + v] = g.bp[y];
-          ++y;
-        }
+        const bool takeA = x < na && (y >= nb || less_pk(AP[x], AK[x], BP[y], BK[y]));
+        rk[v] = takeA ? AK[x] : BK[y];
+        rp[v] = takeA ? AP[x] : BP[y];
+        x += takeA;
+        y += !takeA;
       }
     }
     if (d0 < d1 && d1 == n) g.ta = x;
-    Bk::sync();
-    for (u32 i = tid; i < n; i += NT) J.sink.put(out + i, g.ok[i], g.op[i]);
+    if (!filter) {
+#pragma unroll
+      for (u32 v = 0; v < VT; ++v)
+        if (d0 + v < d1) {
+          g.ok[d0 + v] = rk[v];
+          g.op[d0 + v] = rp[v];
+        }
+      Bk::sync();
+      for (u32 i = tid; i < n; i += NT) J.sink.put(out + i, g.ok[i], g.op[i]);
+      written += n;
+    } else {
+      // drop stale entries (primitives.cpp:103-120 semantics through the
+      // position index): the survivors keep their merged order, compacted
+      // by a CTA scan into the staging tile
+      u32 keepm = 0;
+#pragma unroll
+      for (u32 v = 0; v < VT; ++v)
+        if (d0 + v < d1 && entry_valid(J.idx, rk[v], rp[v])) keepm |= 1u << v;
+      u32 tot;
+      u32 pos = Bk::scan_excl(__popc(keepm), tot, g.scr);
+#pragma unroll
+      for (u32 v = 0; v < VT; ++v)
+        if (keepm >> v & 1u) {
+          g.ok[pos] = rk[v];
+          g.op[pos] = rp[v];
+          ++pos;
+        }
+      Bk::sync();
+      for (u32 i = tid; i < tot; i += NT) J.sink.put(out + written + i, g.ok[i], g.op[i]);
+      written += tot;
+    }
     const u32 ta = g.ta;
     ia += ta;
     ib += n - ta;
-    out += n;
+    if (!filter) out += n;
     Bk::sync();
   }
+  if (tid == 0) g.mph = ph;
+  return written;
+}
+
+// Valid entries (index check) in (k, p)[i0, i1): CTA-wide count.
+template <int NT>
+DEV u32 count_valid(const u32* k, const u64* p, u32 i0, u32 i1, const pbh_idx_entry* idx, u32* scr) {
+  u32 c = 0;
+  for (u32 i = i0 + threadIdx.x; i < i1; i += NT) c += entry_valid(idx, k[i], p[i]);
+  return Blk<NT>::sum(c, scr);
 }
 
 // Warp-aggregated append to a global counter: returns this lane's slot.
@@ -447,14 +536,15 @@ DEV void batch_merge_pass(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g, u32* scrat
     const Run A{X->sk[s] + base, X->sp[s] + base, na};
     const Run B{X->sk[s] + base + na, X->sp[s] + base + na, nb};
     const u32 d0 = lo - base, d1 = hi - base;
-    const u32 a0 = d0 == 0 ? 0 : merge_split<NT>(A, B, d0, scratch);
-    const u32 a1 = merge_split<NT>(A, B, d1, scratch);
+    u32 a0, a1;
+    merge_split2<NT>(A, B, d0, d1, scratch, a0, a1);
     if (threadIdx.x == 0) {
       g.sub.ak = A.k;
       g.sub.ap = A.p;
       g.sub.bk = B.k;
       g.sub.bp = B.p;
       g.sub.sink = Sink{X->sk[s ^ 1] + base, X->sp[s ^ 1] + base, 0xffffffffu, nullptr, nullptr};
+      g.sub.filter = 0;
     }
     Blk<NT>::sync();
     grid_stream<NT>(g.sub, a0, a1, d0 - a0, d1 - a1, d0, g);
@@ -464,26 +554,22 @@ DEV void batch_merge_pass(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g, u32* scrat
 }
 
 // Barrier over the G CTAs of a job (all co-resident: cooperative launch).
-// Sense by generation: read the generation, arrive; the last arrival resets
-// the count and publishes the next generation.
+// One monotone arrival counter per launch (zeroed by the host before the
+// launch): barrier e of the launch completes when the counter reaches
+// (e + 1) * G; every CTA passes the same barriers, so each tracks e locally.
+// Arrival is a fire-and-forget release reduction; waiting is an acquire poll.
 template <int NT>
-DEV void job_barrier(BatchJob* X, u32 G) {
+DEV void job_barrier(BatchJob* X, u32 G, GridSmem<NT>& g) {
   Blk<NT>::sync();
   if (threadIdx.x == 0) {
-    const u32 gen = ld_acquire(&X->bar_gen);
-    __threadfence();
-    if (atomicAdd(&X->bar_cnt, 1u) == G - 1) {
-      X->bar_cnt = 0;
-      __threadfence();
-      st_release(&X->bar_gen, gen + 1);
-    } else {
-      u32 backoff = 16;
-      while (ld_acquire(&X->bar_gen) == gen) {
-        __nanosleep(backoff);
-        backoff = backoff < kPollMaxNs ? backoff * 2 : kPollMaxNs;
-      }
+    const u32 target = (g.bar_epoch + 1) * G;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(&X->bar_cnt) : "memory");
+    u32 backoff = 8;
+    while ((int)(ld_acquire(&X->bar_cnt) - target) < 0) {
+      __nanosleep(backoff);
+      backoff = backoff < kPollMaxNs ? backoff * 2 : kPollMaxNs;
     }
-    __threadfence();
+    g.bar_epoch += 1;
   }
   Blk<NT>::sync();
 }
@@ -496,8 +582,17 @@ DEV void job_barrier(BatchJob* X, u32 G) {
 // is published by the sort job, once the whole batch is known to be valid).
 // The staged priorities' range feeds the bucket sort.
 template <int NT>
-DEV void batch_check_classify(BatchJob* X, u32 b, u32 G) {
-  const u32 n = X->n;
+DEV void batch_check_classify(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
+  // the descriptor in registers (stores below could alias it for the compiler)
+  const u32 n = X->n, c0 = X->c0, spl_k = X->spl_k;
+  const bool check = X->check, debug = X->debug, spl_inf = X->spl_inf;
+  const u64 universe = X->universe, spl_p = X->spl_p;
+  const u32* __restrict__ vals = X->vals;
+  const u64* __restrict__ prios = X->prios;
+  const pbh_idx_entry* idx = X->idx;
+  u32* ll = X->ll;
+  u32* stg_k = X->stg_k;
+  u64* stg_p = X->stg_p;
   const u32 r0 = (u32)((u64)n * b / G), r1 = (u32)((u64)n * (b + 1) / G);
   u32 fresh = 0, bad = 0;
   u64 lo = ~0ull, hi = 0;
@@ -507,20 +602,20 @@ DEV void batch_check_classify(BatchJob* X, u32 b, u32 G) {
     u32 k = 0;
     u64 p = 0;
     if (j < r1) {
-      k = X->vals[j];
-      p = X->prios[j];
-      if (X->check && j > 0 && X->vals[j - 1] >= k) bad |= 1;
-      if (k >= X->universe) {
+      k = vals[j];
+      p = prios[j];
+      if (check && j > 0 && vals[j - 1] >= k) bad |= 1;
+      if (k >= universe) {
         bad |= 2;
       } else {
-        const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(X->idx + k));
+        const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + k));
         const u32 st = (u32)e.y;
         if (PBH_ST(st) == PBH_ST_DEAD) bad |= 4;
-        if (X->debug && PBH_ST(st) == PBH_ST_LIVE && p > e.x) bad |= 8;
+        if (debug && PBH_ST(st) == PBH_ST_LIVE && p > e.x) bad |= 8;
         const bool fr = PBH_ST(st) != PBH_ST_LIVE;
         if (fr || p < e.x) {
-          const bool adm = X->spl_inf || p < X->spl_p || (p == X->spl_p && k <= X->spl_k);
-          if ((!fr && (st >> 2) < X->c0) || adm) {
+          const bool adm = spl_inf || p < spl_p || (p == spl_p && k <= spl_k);
+          if ((!fr && (st >> 2) < c0) || adm) {
             to_leader = true;
           } else {
             to_hbm = true;
@@ -531,13 +626,23 @@ DEV void batch_check_classify(BatchJob* X, u32 b, u32 G) {
         }
       }
     }
-    const u32 ls = warp_append(&X->ll_n, to_leader);
-    if (to_leader) X->ll[ls] = j;
-    const u32 hs = warp_append(&X->stg_n, to_hbm);
-    if (to_hbm) {
-      X->stg_k[hs] = k;
-      X->stg_p[hs] = p;
+    // one reservation per CTA and counter per step (a contended global
+    // counter per warp costs more than the CTA scan): leader-list count in
+    // the low 16 bits, staging count in the high 16 bits
+    u32 tot;
+    const u32 mine = Blk<NT>::scan_excl((to_leader ? 1u : 0u) | (to_hbm ? 1u << 16 : 0u), tot, g.scr);
+    if (threadIdx.x == 0) {
+      g.ok[0] = (tot & 0xffffu) ? atomicAdd(&X->ll_n, tot & 0xffffu) : 0u;
+      g.ok[1] = (tot >> 16) ? atomicAdd(&X->stg_n, tot >> 16) : 0u;
     }
+    Blk<NT>::sync();
+    if (to_leader) ll[g.ok[0] + (mine & 0xffffu)] = j;
+    if (to_hbm) {
+      const u32 hs = g.ok[1] + (mine >> 16);
+      stg_k[hs] = k;
+      stg_p[hs] = p;
+    }
+    Blk<NT>::sync();
   }
   fresh = __reduce_add_sync(0xffffffffu, fresh);
   bad = __reduce_or_sync(0xffffffffu, bad);
@@ -570,6 +675,7 @@ DEV void batch_bucket_sort(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
   const u32 n = X->stg_n, NB = X->nbkt;
   const u64 pmin = X->pmin, width = X->bwidth;
   const u32 r0 = (u32)((u64)n * b / G), r1 = (u32)((u64)n * (b + 1) / G);
+  long long tp = clock64();
   u32* cnt = reinterpret_cast<u32*>(g.op);  // NB per-CTA counts, then cursors
   u32* base = cnt + kBucketMax;              // NB bases (this CTA's offset in a bucket)
   u32* start = base + kBucketMax;            // NB bucket starts
@@ -585,7 +691,9 @@ DEV void batch_bucket_sort(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
     base[i] = c ? atomicAdd(&X->bcnt[i], c) : 0;
     cnt[i] = 0;  // becomes the scatter cursor
   }
-  job_barrier<NT>(X, G);
+  if (b == 0) { jobprof_add(8, clock64() - tp); tp = clock64(); }
+  job_barrier<NT>(X, G, g);
+  if (b == 0) { jobprof_add(9, clock64() - tp); tp = clock64(); }
   // bucket starts: exclusive scan of the totals (every CTA, NB <= kBucketMax)
   {
     u32 run = 0;
@@ -601,6 +709,8 @@ DEV void batch_bucket_sort(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
   Bk::sync();
   u32* DK = X->sk[1];
   u64* DP = X->sp[1];
+  const bool write_idx = X->write_idx;
+  pbh_idx_entry* idx = X->idx;
   for (u32 j = r0 + threadIdx.x; j < r1; j += NT) {
     const u32 k = SK[j];
     const u64 p = SP[j];
@@ -608,15 +718,17 @@ DEV void batch_bucket_sort(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
     const u32 pos = start[q] + base[q] + atomicAdd(&cnt[q], 1u);
     DK[pos] = k;
     DP[pos] = p;
-    if (X->write_idx) {
+    if (write_idx) {
       pbh_idx_entry ne;
       ne.prio = p;
       ne.state = PBH_ST_LIVE | (PBH_LOC_DEEP << 2);
       ne.parent = 0;
-      reinterpret_cast<ulonglong2*>(X->idx)[k] = *reinterpret_cast<const ulonglong2*>(&ne);
+      reinterpret_cast<ulonglong2*>(idx)[k] = *reinterpret_cast<const ulonglong2*>(&ne);
     }
   }
-  job_barrier<NT>(X, G);
+  if (b == 0) { jobprof_add(10, clock64() - tp); tp = clock64(); }
+  job_barrier<NT>(X, G, g);
+  if (b == 0) { jobprof_add(11, clock64() - tp); tp = clock64(); }
   for (u32 q = b; q < NB; q += G) {
     const u32 m = __ldcg(&X->bcnt[q]), s0 = start[q];
     if (m > kGridTile) {
@@ -624,6 +736,44 @@ DEV void batch_bucket_sort(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
       continue;
     }
     if (m < 2) continue;
+    if (m <= kRankSortMax) {
+      // small bucket: rank sort ((p, k) pairs are unique: a key's copies
+      // have distinct priorities), each thread ranks up to two entries
+      // against the bucket in shared memory and stores them in place
+      u32 k0 = 0, k1 = 0;
+      u64 p0 = 0, p1 = 0;
+      const u32 i0 = threadIdx.x, i1 = threadIdx.x + NT;
+      if (i0 < m) {
+        k0 = DK[s0 + i0];
+        p0 = DP[s0 + i0];
+        g.ak[i0] = k0;
+        g.ap[i0] = p0;
+      }
+      if (i1 < m) {
+        k1 = DK[s0 + i1];
+        p1 = DP[s0 + i1];
+        g.ak[i1] = k1;
+        g.ap[i1] = p1;
+      }
+      Bk::sync();
+      u32 r0 = 0, r1 = 0;
+      for (u32 j = 0; j < m; ++j) {
+        const u64 pj = g.ap[j];
+        const u32 kj = g.ak[j];
+        r0 += less_pk(pj, kj, p0, k0);
+        r1 += less_pk(pj, kj, p1, k1);
+      }
+      if (i0 < m) {
+        DK[s0 + r0] = k0;
+        DP[s0 + r0] = p0;
+      }
+      if (i1 < m) {
+        DK[s0 + r1] = k1;
+        DP[s0 + r1] = p1;
+      }
+      Bk::sync();
+      continue;
+    }
     for (u32 i = threadIdx.x; i < m; i += NT) {
       cp_async4(&g.ak[i], DK + s0 + i, true);
       cp_async8(&g.ap[i], DP + s0 + i);
@@ -638,6 +788,7 @@ DEV void batch_bucket_sort(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
     }
     Bk::sync();
   }
+  if (b == 0) jobprof_add(12, clock64() - tp);
 }
 
 // This CTA's share (block b of G) of the current job.
@@ -649,15 +800,46 @@ DEV void grid_share(const GridJob& J, u32 b, GridSmem<NT>& g, u32* scratch) {
     case 3: return batch_classify<NT>(J.ext, b, G);
     case 4: return batch_sort_chunks<NT>(J.ext, b, G, g);
     case 5: return batch_merge_pass<NT>(J.ext, b, G, g, scratch);
-    case 6: return batch_check_classify<NT>(J.ext, b, G);
+    case 6: return batch_check_classify<NT>(J.ext, b, G, g);
     case 7: return batch_bucket_sort<NT>(J.ext, b, G, g);
     default: break;
   }
   const u32 r0 = (u32)((u64)J.c * b / G), r1 = (u32)((u64)J.c * (b + 1) / G);
-  if (r0 >= r1) return;
   const Run A{J.ak, J.ap, J.na}, B{J.bk, J.bp, J.nb};
-  const u32 a0 = r0 == 0 ? 0 : merge_split<NT>(A, B, r0, scratch);
-  const u32 a1 = merge_split<NT>(A, B, r1, scratch);
+  if (J.kind == 8) {
+    // filtered merge: (1) each CTA counts the valid entries of its input
+    // ranges; (2) after a grid barrier, the exclusive prefix of the counts
+    // is its output start and it streams its range, dropping stale entries
+    BatchJob* X = J.ext;
+    u32 a0 = 0, a1 = 0;
+    if (r0 < r1) merge_split2<NT>(A, B, r0, r1, scratch, a0, a1);
+    const u32 mine = r0 < r1 ? count_valid<NT>(A.k, A.p, a0, a1, J.idx, scratch) +
+                                   count_valid<NT>(B.k, B.p, r0 - a0, r1 - a1, J.idx, scratch)
+                             : 0u;
+    if (threadIdx.x == 0) X->bcnt[b] = mine;
+    job_barrier<NT>(X, G, g);
+    u32 start = 0;
+    {
+      u32 run = 0;
+      for (u32 i0 = 0; i0 < G; i0 += NT) {
+        const u32 i = i0 + threadIdx.x;
+        const u32 v = i < G ? __ldcg(&X->bcnt[i]) : 0u;
+        u32 tot;
+        const u32 e = run + Blk<NT>::scan_excl(v, tot, scratch);
+        if (i == b) g.ok[0] = e;
+        if (b == 0 && i0 + NT >= G && threadIdx.x == 0) X->merge_total = run + tot;
+        run += tot;
+      }
+      Blk<NT>::sync();
+      start = g.ok[0];
+      Blk<NT>::sync();
+    }
+    if (r0 < r1) grid_stream<NT>(J, a0, a1, r0 - a0, r1 - a1, J.out_base + start, g);
+    return;
+  }
+  if (r0 >= r1) return;
+  u32 a0, a1;
+  merge_split2<NT>(A, B, r0, r1, scratch, a0, a1);
   grid_stream<NT>(J, a0, a1, r0 - a0, r1 - a1, J.out_base + r0, g);
 }
 
@@ -666,8 +848,7 @@ template <int NT>
 DEV void grid_helper_loop(GridJob* gj, GridSmem<NT>& g, u32* scratch) {
   using Bk = Blk<NT>;
   u32 seen = 0;
-  if (threadIdx.x == 0) g.seq = 0;
-  Bk::sync();
+  grid_smem_init<NT>(g);
   for (;;) {
     if (threadIdx.x == 0) {
       u32 s;
@@ -677,11 +858,15 @@ DEV void grid_helper_loop(GridJob* gj, GridSmem<NT>& g, u32* scratch) {
         backoff = backoff < kPollMaxNs ? backoff * 2 : kPollMaxNs;
       }
       g.seq = s;
-      // the descriptor, read through L2 (never a stale L1 line)
-      static_assert(sizeof(GridJob) % 8 == 0, "GridJob is copied as 8-byte words");
+    }
+    Bk::sync();
+    {
+      // the descriptor, one 8-byte word per thread, read through L2 (never
+      // a stale L1 line), ordered after thread 0's acquire by the barrier
+      static_assert(sizeof(GridJob) % 8 == 0 && sizeof(GridJob) / 8 <= NT, "GridJob words");
       const unsigned long long* src = reinterpret_cast<const unsigned long long*>(gj);
       unsigned long long* dst = reinterpret_cast<unsigned long long*>(&g.job);
-      for (u32 i = 0; i < sizeof(GridJob) / 8; ++i) dst[i] = __ldcg(src + i);
+      if (threadIdx.x < sizeof(GridJob) / 8) dst[threadIdx.x] = __ldcg(src + threadIdx.x);
     }
     Bk::sync();
     seen = g.seq;
@@ -698,7 +883,7 @@ DEV void grid_helper_loop(GridJob* gj, GridSmem<NT>& g, u32* scratch) {
 // Leader: call once at kernel start (the host zeroed the job word).
 template <int NT>
 DEV void grid_leader_init(GridSmem<NT>& g) {
-  if (threadIdx.x == 0) g.seq = 0;
+  (void)g;  // grid_smem_init ran at kernel start
 }
 
 // Leader side: publish (kind, runs, sink), take share 0, wait for the rest.
@@ -706,6 +891,7 @@ template <int NT>
 NOINL void grid_run(GridJob* gj, u32 G, u32 kind, const Run& A, const Run& B, u32 c,
                     const Sink& sink, u32 out_base, GridSmem<NT>& g, u32* scratch) {
   using Bk = Blk<NT>;
+  const long long t_job = clock64();
   Bk::sync();
   if (threadIdx.x == 0) {
     GridJob& J = g.job;
@@ -721,6 +907,8 @@ NOINL void grid_run(GridJob* gj, u32 G, u32 kind, const Run& A, const Run& B, u3
     J.out_base = out_base;
     J.sink = sink;
     J.ext = g.job.ext;
+    J.filter = kind == 8 ? 1u : 0u;
+    J.idx = g.job.idx;
     // descriptor fields first, then the sequence word (release)
     gj->kind = J.kind;
     gj->nblk = J.nblk;
@@ -734,6 +922,8 @@ NOINL void grid_run(GridJob* gj, u32 G, u32 kind, const Run& A, const Run& B, u3
     gj->out_base = J.out_base;
     gj->sink = J.sink;
     gj->ext = J.ext;
+    gj->idx = J.idx;
+    gj->filter = J.filter;
     gj->done = 0;
     const u32 s = g.seq + 1;  // the host zeroes the job word before each launch
     g.seq = s;
@@ -743,6 +933,7 @@ NOINL void grid_run(GridJob* gj, u32 G, u32 kind, const Run& A, const Run& B, u3
   Bk::sync();
   if (kind == 1) return;
   grid_share<NT>(g.job, 0, g, scratch);
+  const long long t_share = clock64();
   Bk::sync();
   if (threadIdx.x == 0) {
     u32 backoff = 16;
@@ -753,6 +944,8 @@ NOINL void grid_run(GridJob* gj, u32 G, u32 kind, const Run& A, const Run& B, u3
     __threadfence();
   }
   Bk::sync();
+  jobprof_add(kind == 8 ? 14u : kind, clock64() - t_job);
+  jobprof_add(13, clock64() - t_share);  // leader waiting for the helpers
 }
 
 }  // namespace pbh_dev

@@ -9,6 +9,11 @@
 namespace pbh_dev {
 
 constexpr u32 kInfCount = 0xffffffffu;
+// Stale shares of the deep content above which the grid (two gather passes)
+// and the streamed (one pass) merges drop stale entries (measured: below
+// them the gathers cost more than the carried entries, C1 and C4).
+constexpr u32 kGridFilterNum = 3, kGridFilterDen = 4;
+constexpr u32 kStreamFilterNum = 3, kStreamFilterDen = 4;
 
 template <int NT, int VT>
 struct HeapSmem {
@@ -18,6 +23,7 @@ struct HeapSmem {
   u32 scratch[NT / 32 + 2];
   i64 live;
   u64 ops;
+  u64 stale_dropped;
   u64 resolves[PBH_MAX_LEVELS];
   u64 touches[PBH_MAX_LEVELS];
   u32 n_levels, d, cap0, debug;
@@ -59,7 +65,9 @@ struct HeapCta {
   DEV static bool hbm_sink(const Sink& k) { return hbm(k.k1) && (k.lim == kInfCount || hbm(k.k2)); }
   // This CTA alone streams the merge through the GridSmem windows
   // (unfiltered; cp.async window loads).
-  NOINL void stream_local(const Run& A, const Run& B, const Sink& snk, u32 out_base) {
+  // Returns the entries written (fewer than A.n + B.n when filtering).
+  NOINL u32 stream_local(const Run& A, const Run& B, const Sink& snk, u32 out_base,
+                         bool filter = false) {
     Bk::sync();
     if (threadIdx.x == 0) {
       GridJob& J = gs->job;
@@ -71,21 +79,48 @@ struct HeapCta {
       J.nb = B.n;
       J.c = A.n + B.n;
       J.sink = snk;
+      J.filter = filter ? 1u : 0u;
+      J.idx = idx;
     }
     Bk::sync();
-    grid_stream<NT>(gs->job, 0, A.n, 0, B.n, out_base, *gs);
+    const u32 n = grid_stream<NT>(gs->job, 0, A.n, 0, B.n, out_base, *gs);
     Bk::sync();
+    return n;
+  }
+  // A filtered merge on the grid (job 8: count, prefix, compacting streams)
+  // needs the job block of the grid sorts for its barrier and counts.
+  DEV bool grid_filter_ok() const { return gs->job.ext != nullptr; }
+  // Stale-entry filtering costs one index gather (a 32-byte sector) per
+  // entry, per pass, and saves the stale entries' traffic through the
+  // deeper merges; it pays only when a good part of the deep content is
+  // stale. The heap's own counters estimate that share with no memory
+  // traffic: entries stored below level 0 minus live values (an
+  // underestimate while level 0 holds live values). True above num/den.
+  DEV u32 dropped(u32 in, u32 out) {
+    if (t0()) s.stale_dropped += in - out;
+    return out;
+  }
+  DEV bool stale_share_above(u32 num, u32 den) const {
+    const u64 stored = content_from(1);
+    const u64 lv = s.live > 0 ? (u64)s.live : 0ull;
+    const u64 stale = stored > lv ? stored - lv : 0ull;
+    return stale * den > (u64)num * stored;
   }
   NOINL u32 mrg(const Run& A, const Run& B, bool filter, const Sink& snk, u32 out_base) {
     const u32 tot = A.n + B.n;
     const bool mem = gs && hbm(A.k) && hbm(B.k) && hbm_sink(snk);
     if (mem && gj && tot >= gmin) {
+      // two gather passes (count, then compacting stream): at least half stale
+      if (filter && grid_filter_ok() && stale_share_above(kGridFilterNum, kGridFilterDen)) {
+        grid_run<NT>(gj, gsz, 8, A, B, tot, snk, out_base, *gs, gs->scr);
+        return dropped(tot, *(volatile u32*)&gs->job.ext->merge_total);
+      }
       grid_run<NT>(gj, gsz, 0, A, B, tot, snk, out_base, *gs, gs->scr);
       return tot;
     }
     if (mem && tot >= kStreamMin) {
-      stream_local(A, B, snk, out_base);
-      return tot;
+      const bool f = filter && stale_share_above(kStreamFilterNum, kStreamFilterDen);
+      return dropped(tot, stream_local(A, B, snk, out_base, f));
     }
     return merge_runs<NT, VT>(A, B, filter, idx, snk, out_base, s.tile, scr());
   }
@@ -93,12 +128,16 @@ struct HeapCta {
     const Run E{A.k, A.p, 0};
     const bool mem = gs && hbm(A.k) && hbm_sink(snk);
     if (mem && gj && A.n >= gmin) {
+      if (filter && grid_filter_ok() && stale_share_above(kGridFilterNum, kGridFilterDen)) {
+        grid_run<NT>(gj, gsz, 8, A, E, A.n, snk, out_base, *gs, gs->scr);
+        return dropped(A.n, *(volatile u32*)&gs->job.ext->merge_total);
+      }
       grid_run<NT>(gj, gsz, 0, A, E, A.n, snk, out_base, *gs, gs->scr);
       return A.n;
     }
     if (mem && A.n >= kStreamMin) {
-      stream_local(A, E, snk, out_base);
-      return A.n;
+      const bool f = filter && stale_share_above(kStreamFilterNum, kStreamFilterDen);
+      return dropped(A.n, stream_local(A, E, snk, out_base, f));
     }
     return copy_run<NT, VT>(A, filter, idx, snk, out_base, scr());
   }
@@ -148,6 +187,7 @@ struct HeapCta {
     if (t0()) {
       s.live = gh->live;
       s.ops = gh->ops;
+      s.stale_dropped = gh->stale_dropped;
       s.n_levels = gh->n_levels;
       s.d = gh->d;
       s.cap0 = gh->cap0;
@@ -210,6 +250,7 @@ struct HeapCta {
     if (t0()) {
       g->live = s.live;
       g->ops = s.ops;
+      g->stale_dropped = s.stale_dropped;
     }
     Bk::sync();
   }

@@ -77,6 +77,9 @@ typedef struct {
   // shadow_dead_ set does (bucket_heap.cpp:55-58,113-125)
   uint32_t* oor_del;
   uint32_t oor_n, oor_cap;
+  // stale entries dropped by the filtered grid / streamed merges (the
+  // CTA-local tile merges near level 0 always filter and are not counted)
+  uint64_t stale_dropped;
 } pbh_heap_dev;
 
 // Op stream (trace_format.hpp:16-33) in device memory.

@@ -150,6 +150,13 @@ class Engine:
         n = nl.value
         return Metrics(ops.value, [int(x) for x in res[:n]], [int(x) for x in tch[:n]])
 
+    def stats(self) -> dict:
+        """pbh_heap_stats: entries stored below level 0 and stale entries
+        dropped by the filtered deep merges (extension)."""
+        st, dr = C.c_uint64(), C.c_uint64()
+        raise_for(_lib.lib().pbh_heap_stats(self._h, C.byref(st), C.byref(dr)))
+        return {"stored_deep": st.value, "stale_dropped": dr.value}
+
     def check_invariants(self) -> list:
         n = C.c_uint64()
         raise_for(_lib.lib().pbh_heap_check_invariants(self._h, C.byref(n)))

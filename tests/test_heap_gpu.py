@@ -278,3 +278,53 @@ def test_run_ops_matches_run_trace(pbh, O, d):
         assert eng.live_size() == n_left
     finally:
         eng.close()
+
+
+def _decrease_storm(n_keys, d, rounds, seed):
+    """Fresh keys, then `rounds` passes of strict decreases over all keys in
+    batches of d, then extract everything: most stored entries go stale."""
+    rng = np.random.default_rng(seed)
+    p = rng.integers(1 << 30, 1 << 31, n_keys).astype(np.uint64)
+    kinds, offs, vals, prios = [], [0], [], []
+
+    def bulk(ks):
+        kinds.append(ord("B"))
+        vals.append(ks.astype(np.uint32))
+        prios.append(p[ks].copy())
+        offs.append(offs[-1] + len(ks))
+    for b in range(0, n_keys, d):
+        bulk(np.arange(b, min(n_keys, b + d)))
+    for _ in range(rounds):
+        for b in range(0, n_keys, d):
+            ks = np.arange(b, min(n_keys, b + d))
+            p[ks] -= rng.integers(1, 1000, len(ks)).astype(np.uint64)
+            bulk(ks)
+    for _ in range(n_keys):
+        kinds.append(ord("E"))
+        offs.append(offs[-1])
+    from oracle import oracle as O
+    return O.Trace(np.array(kinds, np.uint8), np.array(offs, np.uint64),
+                   np.concatenate(vals), np.concatenate(prios))
+
+
+@pytest.mark.parametrize("n_keys,d,rounds", [(1 << 14, 1024, 12), (1 << 16, 16384, 8)])
+def test_filtered_deep_merges_drop_stale(pbh, O, n_keys, d, rounds):
+    # repeated decreases of every key make most deep entries stale: the
+    # streamed (d=1024) and grid (d=16384) merges then drop them through the
+    # position index, and the extraction sequence stays the oracle's
+    tr = _decrease_storm(n_keys, d, rounds, 7)
+    want_v, want_p = O.run_oracle(tr)
+    eng = pbh.Engine(pbh.EngineConfig(d=d, debug_assertions=False, key_universe=n_keys))
+    try:
+        k = int(np.nonzero(tr.kinds == ord("E"))[0][0])
+        head = O.Trace(tr.kinds[:k], tr.offsets[:k + 1], tr.vals, tr.prios)
+        eng.run_ops(head)
+        st = eng.stats()
+        assert st["stale_dropped"] > 0, st
+        tail = O.Trace(tr.kinds[k:], tr.offsets[k:] - tr.offsets[k], tr.vals[:0], tr.prios[:0])
+        got = eng.run_trace(tail)
+        assert np.array_equal(got.extracted_values, want_v)
+        assert np.array_equal(got.extracted_priorities, want_p)
+        assert eng.check_invariants() == []
+    finally:
+        eng.close()
