@@ -60,7 +60,7 @@ def parse(argv=None):
     ap.add_argument("--impl", default="pbh", choices=["pbh", "reference"])
     ap.add_argument("--sources", type=int, default=64, help="C5 sources in total")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--legs", default="c3,c2,c1,c4",
+    ap.add_argument("--legs", default="c3,c2,c1,c4,api",
                     help="extra BASELINE configs measured on rank 0 (comma list, or 'none')")
     ap.add_argument("--c1-ops", type=int, default=200_000)
     ap.add_argument("--c4-ds", default="32,256,1024,8192,65536")
@@ -499,6 +499,45 @@ def leg_c4(P, gen, dev, peak, ds, cpu):
     return out
 
 
+def leg_api_latency(P, dev, n_calls=2000):
+    """Per-call cost of the single-client Engine API through the C-ABI
+    (engine.cpp:90-109: update, bulk_update, extract_min, delete_value): host
+    wall time per blocking call, heap of 2^20 keys at d = 32 (the latency
+    regime). Calls go through the Python ctypes mirror, so each includes
+    ~1-2 us of interpreter overhead."""
+    import time as _t
+    warm = P.Engine(P.EngineConfig(d=32, debug_assertions=False, key_universe=1 << 10, device=dev))
+    for i in range(64):  # first launches (module load) outside the timing
+        warm.update((i, 10 + i))
+        warm.extract_min()
+    warm.close()
+    eng = P.Engine(P.EngineConfig(d=32, debug_assertions=False, key_universe=1 << 20, device=dev))
+    rng = np.random.default_rng(3)
+    keys = rng.permutation(1 << 20).astype(np.uint32)
+    out = {}
+    t0 = _t.perf_counter()
+    for i in range(n_calls):
+        eng.update((int(keys[i]), int(1000 + i)))
+    out["update_us"] = (_t.perf_counter() - t0) * 1e6 / n_calls
+    batches = [np.sort(keys[n_calls + 32 * i:n_calls + 32 * (i + 1)]) for i in range(n_calls)]
+    pr = np.arange(32, dtype=np.uint64) + 5000
+    t0 = _t.perf_counter()
+    for b in batches:
+        eng.bulk_update(values=b, priorities=pr)
+    out["bulk_update_d32_us"] = (_t.perf_counter() - t0) * 1e6 / n_calls
+    t0 = _t.perf_counter()
+    for _ in range(n_calls):
+        eng.extract_min()
+    out["extract_min_us"] = (_t.perf_counter() - t0) * 1e6 / n_calls
+    t0 = _t.perf_counter()
+    for i in range(n_calls):
+        eng.delete_value(int(keys[i]))
+    out["delete_us"] = (_t.perf_counter() - t0) * 1e6 / n_calls
+    eng.close()
+    out["calls_each"] = n_calls
+    return out
+
+
 # ------------------------------------------------------------- GPU arm
 def run_pbh(args, D):
     import paper_1908_09378_b200 as P
@@ -667,6 +706,8 @@ def run_pbh(args, D):
         legs["c2_grid"] = leg_c2(P, gen, dev, peak, G.get("C2"), run_cpu)
     if "c1" in which:
         legs["c1_op_trace"] = leg_c1(P, gen, dev, peak, args.c1_ops, G.get("C1"), run_cpu)
+    if "api" in which:
+        legs["api_latency"] = leg_api_latency(P, dev)
     if "c4" in which:
         legs["c4_bulk_update"] = leg_c4(P, gen, dev, peak, [int(x) for x in args.c4_ds.split(",")],
                                         run_cpu)

@@ -1161,6 +1161,35 @@ struct TraceBankSmem {
   GridSmem<32 * NW> g;
 };
 
+// Level-0 image transfer of the op-trace engine (shared memory <-> HBM):
+// everything except the SSSP row fields, and only the filled prefix of the
+// push buffer. `to_smem`: the image is the source (its qn is read first).
+template <int B, int KI>
+DEV void trace_image_copy(BankL0<B, KI>& dst, const BankL0<B, KI>& src, bool to_smem) {
+  constexpr u32 C0 = B * KI;
+  const u32 tid = threadIdx.x;
+  for (u32 i = tid; i < C0; i += B) {
+    dst.lp[i] = src.lp[i];
+    dst.lk[i] = src.lk[i];
+  }
+  dst.occ[tid] = src.occ[tid];
+  if (tid == 0) {
+    dst.spl_p = src.spl_p;
+    dst.spl_k = src.spl_k;
+    dst.spl_inf = src.spl_inf;
+    dst.qn = src.qn;
+    dst.pad = src.pad;
+    dst.pushes = src.pushes;
+  }
+  __syncthreads();
+  const u32 qn = to_smem ? dst.qn : src.qn;
+  for (u32 i = tid; i < qn; i += B) {
+    dst.qk[i] = src.qk[i];
+    dst.qp[i] = src.qp[i];
+  }
+  __syncthreads();
+}
+
 template <int NW, int KI, int VT>
 __global__ void __launch_bounds__(32 * NW, 1)
     k_trace_bank(pbh_heap_dev* g, pbh_trace_dev tr, u64 op_begin, u64 op_end, u32* out_v,
@@ -1213,12 +1242,11 @@ __global__ void __launch_bounds__(32 * NW, 1)
   // batches beyond the large-batch buffers (2^26 entries) are rejected, not split
   const u32 dmax = min(sm.d, kMaxBatch);
   const bool debug = sm.debug != 0;
-  // restore the level-0 image
-  {
-    const u32* src = reinterpret_cast<const u32*>(save);
-    u32* dst = reinterpret_cast<u32*>(&L);
-    for (u32 i = tid; i < sizeof(BankL0<B, KI>) / 4; i += B) dst[i] = src[i];
-  }
+  // restore the level-0 image: the parts this engine uses (slot keys and
+  // priorities, bank masks, splitter, counters, the filled push-buffer
+  // prefix; the SSSP-only row fields stay behind), which keeps a single-op
+  // launch short
+  trace_image_copy<B, KI>(L, *save, true);
   for (u32 i = tid; i < 2 * B; i += B) (&S.dirty[0][0])[i] = 0;
   Bk::sync();
   H.occm = L.occ[tid];
@@ -1687,11 +1715,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
     L.pushes = H.pushes;
   }
   Bk::sync();
-  {
-    const u32* src = reinterpret_cast<const u32*>(&L);
-    u32* dst = reinterpret_cast<u32*>(save);
-    for (u32 i = tid; i < sizeof(BankL0<B, KI>) / 4; i += B) dst[i] = src[i];
-  }
+  trace_image_copy<B, KI>(*save, L, false);
   H.to_cold();
   hc.store();
   if (tid == 0) {

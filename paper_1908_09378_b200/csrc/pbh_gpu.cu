@@ -46,6 +46,8 @@ pbh_status set_err(pbh_status s, const std::string& msg) {
 constexpr int VT = 4;
 constexpr u32 kOorCap = 4096;  // remembered out-of-index deletes per heap
 constexpr size_t kTmaSlack = 64;  // bytes past each merge buffer (TMA window over-read)
+constexpr u32 kInlineOpMax = 256;  // single ops up to this many elements read from mapped host memory
+constexpr u64 kSoloMax = 1ull << 16;  // single ops on one CTA while fewer entries were inserted
 
 u64 pow2_at_least(u64 x) {
   u64 p = 1;
@@ -76,17 +78,19 @@ using TraceSmem = TraceBankSmem<kTraceNW, kTraceKI, VT>;
 cudaError_t launch_trace_bank(cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr, u64 b, u64 e,
                               u32* ov, u64* op, pbh_kstatus* ks, TraceImage* save, u32 internal,
                               GridJob* gj, u32 grid_min, unsigned long long* prof,
-                              BatchJob* bj) {
+                              BatchJob* bj, bool solo) {
   auto fn = k_trace_bank<kTraceNW, kTraceKI, VT>;
   const int smem = (int)sizeof(TraceSmem);
-  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (err != cudaSuccess) return err;
+  cudaError_t err = cudaSuccess;
   int G = 0;
   {
+    // per device, once: the shared-memory opt-in and the co-resident grid
     const int dev = current_device();
     std::lock_guard<std::mutex> lk(g_attr_mu);
     int& gc = g_grid_of[{(const void*)fn, dev}];
     if (gc == 0) {
+      err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (err != cudaSuccess) return err;
       int sms = 0, per_sm = 0;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kTraceNW, smem);
@@ -94,13 +98,10 @@ cudaError_t launch_trace_bank(cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr
     }
     G = gc;
   }
-  if (gj && G > 1) {
+  if (gj && G > 1 && !solo) {
+    // the job word and the job-barrier counter restart with every launch
     err = cudaMemsetAsync(gj, 0, sizeof(GridJob), st);
     if (err != cudaSuccess) return err;
-    if (bj) {  // the job-barrier counter restarts with every launch
-      err = cudaMemsetAsync(&bj->bar_cnt, 0, sizeof(u32), st);
-      if (err != cudaSuccess) return err;
-    }
     void* args[] = {&g, &tr, &b, &e, &ov, &op, &ks, &save, &internal, &gj, &grid_min, &prof, &bj};
     err = cudaLaunchCooperativeKernel((const void*)fn, dim3(G), dim3(32 * kTraceNW), args, smem, st);
   } else {
@@ -418,8 +419,24 @@ struct pbh_heap {
   u64 d = 1;
   int nt = 32;
   DevHeap H;
-  pbh_kstatus* d_ks = nullptr;
-  pbh_kstatus* h_ks = nullptr;  // pinned
+  pbh_kstatus* d_ks = nullptr;  // device view of h_ks
+  pbh_kstatus* h_ks = nullptr;  // status block in mapped pinned host memory (written by the kernel)
+  // single ops (the Engine's per-call API): their inputs and outputs live in
+  // mapped pinned host memory the kernel reads / writes directly (no copies)
+  struct MappedOp {
+    u8 kinds[16];
+    u64 off[2];
+    u32 vals[kInlineOpMax];
+    u64 prios[kInlineOpMax];
+    u32 out_v[1];
+    u64 out_p[1];
+  };
+  MappedOp* h_mop = nullptr;
+  MappedOp* d_mop = nullptr;
+  // entries inserted so far (an upper bound of what the heap stores): while
+  // small, single ops launch one CTA (their merges are short) instead of
+  // the cooperative grid
+  u64 inserted = 0;
   GridJob* d_job = nullptr;     // grid-helper job word (null: single-CTA engine)
   TraceImage* d_save = nullptr; // its level-0 image between launches
   u32 grid_min = kGridMin;
@@ -470,28 +487,33 @@ pbh_status ensure_staging(pbh_heap* h, u64 n_ops, u64 n_el, u64 n_out) {
 // loop. host_vals: host copy of the values (for universe growth) or null.
 pbh_status exec_trace(pbh_heap* h, u64 n_ops, pbh_trace_dev tr, u32* d_ov, u64* d_op,
                       u64* n_out, u64* failed_op, u32 internal, double* wall_ms,
-                      const u8* host_kinds, const u64* host_off, const u32* host_vals) {
-  CK(cudaMemsetAsync(h->d_ks, 0, sizeof(pbh_kstatus), h->stream));
+                      const u8* host_kinds, const u64* host_off, const u32* host_vals,
+                      bool solo = false) {
+  // the status block is mapped host memory: the stream is idle between
+  // calls, so the host resets it directly and reads the kernel's writes
+  // after the synchronize
+  std::memset(h->h_ks, 0, sizeof(pbh_kstatus));
   u64 begin = 0;
   double ms_total = 0;
   for (int guard = 0; guard < 4096; ++guard) {
     if (begin >= n_ops) break;
-    CK(cudaEventRecord(h->ev0, h->stream));
+    if (wall_ms) CK(cudaEventRecord(h->ev0, h->stream));
     CK(launch_trace_bank(h->stream, h->H.dev, tr, begin, n_ops, d_ov, d_op, h->d_ks, h->d_save,
-                         internal, h->d_job, h->grid_min, h->d_prof, h->d_batch));
-    CK(cudaEventRecord(h->ev1, h->stream));
-    CK(cudaMemcpyAsync(h->h_ks, h->d_ks, sizeof(pbh_kstatus), cudaMemcpyDeviceToHost, h->stream));
+                         internal, h->d_job, h->grid_min, h->d_prof, h->d_batch, solo));
+    if (wall_ms) CK(cudaEventRecord(h->ev1, h->stream));
     CK(cudaStreamSynchronize(h->stream));
-    float ms = 0;
-    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
-    ms_total += ms;
-    const pbh_kstatus ks = *h->h_ks;
+    if (wall_ms) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+      ms_total += ms;
+    }
+    const pbh_kstatus ks = *h->h_ks;  // written by the kernel; visible after the synchronize
     if (ks.status == 0) break;
     if (ks.status == 7) {  // NEED_GROW
       pbh_status st = grow_levels(h->H, h->stream);
       if (st) return st;
       begin = ks.failed_op;
-      CK(cudaMemsetAsync(&h->d_ks->status, 0, 4, h->stream));
+      h->h_ks->status = 0;
       continue;
     }
     if (ks.detail == PBH_ERR_KEY_RANGE) {
@@ -516,7 +538,7 @@ pbh_status exec_trace(pbh_heap* h, u64 n_ops, pbh_trace_dev tr, u32* d_ov, u64* 
       pbh_status st = grow_universe(h->H, h->stream, mx + 1);
       if (st) return st;
       begin = op;
-      CK(cudaMemsetAsync(&h->d_ks->status, 0, 4, h->stream));
+      h->h_ks->status = 0;
       continue;
     }
     if (n_out) *n_out = ks.n_out;
@@ -555,6 +577,7 @@ pbh_status exec_host(pbh_heap* h, u64 n_ops, const u8* kinds, const u64* off, co
   }
   pbh_trace_dev tr{h->d_kinds, h->d_off, h->d_vals, h->d_prios};
   u64 got = 0;
+  h->inserted += n_el;
   pbh_status rs = exec_trace(h, n_ops, tr, h->d_ov, h->d_op, &got, failed_op, internal, wall_ms,
                              kinds, off, vals);
   if (n_out) *n_out = got;
@@ -594,7 +617,30 @@ pbh_status single_op(pbh_heap* h, u8 kind, const u32* vals, const u64* prios, u6
                      u64* op) {
   u64 off[2] = {0, n};
   u64 got = 0;
-  pbh_status st = exec_host(h, 1, &kind, off, vals, prios, ov, op, &got, nullptr, 1, nullptr);
+  pbh_status st;
+  if (n <= kInlineOpMax && !h->d_prof) {
+    // zero-copy: the op and its elements in mapped host memory, the
+    // extraction written straight back there
+    auto* m = h->h_mop;
+    m->kinds[0] = kind;
+    m->off[0] = 0;
+    m->off[1] = n;
+    if (n) {
+      std::memcpy(m->vals, vals, n * 4);
+      std::memcpy(m->prios, prios, n * 8);
+    }
+    pbh_trace_dev tr{h->d_mop->kinds, h->d_mop->off, h->d_mop->vals, h->d_mop->prios};
+    const bool solo = h->inserted + n < kSoloMax;
+    st = exec_trace(h, 1, tr, h->d_mop->out_v, h->d_mop->out_p, &got, nullptr, 1, nullptr,
+                    &kind, off, vals, solo);
+    if (kind == 'U' || kind == 'B') h->inserted += n;
+    if (got && ov) {
+      *ov = const_cast<volatile u32*>(m->out_v)[0];
+      *op = const_cast<volatile u64*>(m->out_p)[0];
+    }
+  } else {
+    st = exec_host(h, 1, &kind, off, vals, prios, ov, op, &got, nullptr, 1, nullptr);
+  }
   if (st == PBH_OK && (kind == 'E' || kind == 'F') && got != 1)
     return set_err(PBH_INVARIANT, "extract produced no element");
   return st;
@@ -639,8 +685,10 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
   while (nlev < 12 && (h->H.base1 << (2 * (nlev - 2))) < 2 * key_universe + 4 * kBankQ) ++nlev;
   pbh_status st = init_heap(h->H, d, cap0, bc, h->nt, key_universe, debug_checks, nlev, nullptr);
   if (st) return fail(st);
-  if (cudaMalloc(&h->d_ks, sizeof(pbh_kstatus)) != cudaSuccess ||
-      cudaMallocHost(&h->h_ks, sizeof(pbh_kstatus)) != cudaSuccess)
+  if (cudaHostAlloc(&h->h_ks, sizeof(pbh_kstatus), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(&h->d_ks, h->h_ks, 0) != cudaSuccess ||
+      cudaHostAlloc(&h->h_mop, sizeof(pbh_heap::MappedOp), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(&h->d_mop, h->h_mop, 0) != cudaSuccess)
     return fail(set_err(PBH_OOM, "status block allocation failed"));
   // grid helpers for the deep merges (PBH_GRID=1 disables them)
   const char* ge = getenv("PBH_GRID");
@@ -700,8 +748,8 @@ pbh_status pbh_heap_destroy(pbh_heap* h) {
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
   h->H.free_all();
-  cudaFree(h->d_ks);
   cudaFreeHost(h->h_ks);
+  cudaFreeHost(h->h_mop);
   cudaFree(h->d_job);
   cudaFree(h->d_save);
   if (h->d_prof) {

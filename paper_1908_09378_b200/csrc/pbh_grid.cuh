@@ -199,7 +199,9 @@ struct GridJob {
   Sink sink;
   BatchJob* ext;
   const pbh_idx_entry* idx;  // stale filter (kind 8, filtered streams): valid iff LIVE at this priority
-  u32 filter, pad_;
+  u32 filter;
+  u32 bar_cnt;     // job-barrier arrivals of the current launch (zeroed with the job word)
+  GridJob* self;   // this descriptor in HBM (for bar_cnt)
 };
 
 // A large bulk_update batch handled by the whole grid (kinds 2-5). The leader
@@ -235,7 +237,6 @@ struct BatchJob {
   u64 pmin, pmax, bwidth;
   u32* bcnt;      // per-bucket element counts (kBucketMax)
   u32 nbkt, bovf; // bucket count; set when a bucket exceeds kGridTile
-  u32 bar_cnt;    // job-barrier arrivals of the current launch (host-zeroed)
   u32 merge_total;  // kind 8: entries written
 };
 constexpr u32 kBucketMax = 1184;  // 8 buckets per CTA of a 148-CTA grid
@@ -560,12 +561,14 @@ DEV void batch_merge_pass(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g, u32* scrat
 // Arrival is a fire-and-forget release reduction; waiting is an acquire poll.
 template <int NT>
 DEV void job_barrier(BatchJob* X, u32 G, GridSmem<NT>& g) {
+  (void)X;
   Blk<NT>::sync();
   if (threadIdx.x == 0) {
+    u32* cnt = &g.job.self->bar_cnt;
     const u32 target = (g.bar_epoch + 1) * G;
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(&X->bar_cnt) : "memory");
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(cnt) : "memory");
     u32 backoff = 8;
-    while ((int)(ld_acquire(&X->bar_cnt) - target) < 0) {
+    while ((int)(ld_acquire(cnt) - target) < 0) {
       __nanosleep(backoff);
       backoff = backoff < kPollMaxNs ? backoff * 2 : kPollMaxNs;
     }
@@ -909,6 +912,7 @@ NOINL void grid_run(GridJob* gj, u32 G, u32 kind, const Run& A, const Run& B, u3
     J.ext = g.job.ext;
     J.filter = kind == 8 ? 1u : 0u;
     J.idx = g.job.idx;
+    J.self = gj;
     // descriptor fields first, then the sequence word (release)
     gj->kind = J.kind;
     gj->nblk = J.nblk;
@@ -924,6 +928,7 @@ NOINL void grid_run(GridJob* gj, u32 G, u32 kind, const Run& A, const Run& B, u3
     gj->ext = J.ext;
     gj->idx = J.idx;
     gj->filter = J.filter;
+    gj->self = gj;
     gj->done = 0;
     const u32 s = g.seq + 1;  // the host zeroes the job word before each launch
     g.seq = s;
