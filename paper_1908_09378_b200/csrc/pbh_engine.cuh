@@ -307,8 +307,9 @@ DEV void tma_load_1d(void* dst, const void* src, u32 bytes, u64* bar) {
 // and the copy size.
 template <int E>
 struct Window {
-  const void* src;
-  u32 off, bytes;
+  const void* src = nullptr;
+  u32 off = 0, bytes = 0;
+  Window() = default;
   DEV Window(const void* base, u32 i, u32 n) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(base) + (uintptr_t)i * E;
     const uintptr_t a0 = a & ~uintptr_t(15);

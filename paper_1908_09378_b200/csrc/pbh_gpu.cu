@@ -595,13 +595,14 @@ void prof_report(pbh_heap* h, const char* when) {
   unsigned long long pc[16];
   if (cudaMemcpy(pc, h->d_prof, sizeof pc, cudaMemcpyDeviceToHost) != cudaSuccess) return;
   cudaMemset(h->d_prof, 0, sizeof pc);
-  unsigned long long jp[16][2];
+  unsigned long long jp[24][2];
   if (cudaMemcpyFromSymbol(jp, g_jobprof, sizeof jp) == cudaSuccess) {
-    static const char* names[16] = {"merge", "exit", "validate", "classify", "chunks", "pass",
+    static const char* names[24] = {"merge", "exit", "validate", "classify", "chunks", "pass",
                                     "check+classify", "bucket_sort", "b:hist", "b:bar1", "b:scatter",
-                                    "b:bar2", "b:sort", "leader_wait", "filtered_merge", "-"};
+                                    "b:bar2", "b:sort", "leader_wait", "filtered_merge", "-",
+                                    "m:split", "m:stream", "s:tma_wait", "s:merge", "s:store", "-", "-", "-"};
     fprintf(stderr, "pbh_jobprof[%s]:", when);
-    for (int i = 0; i < 15; ++i)
+    for (int i = 0; i < 24; ++i)
       if (jp[i][1]) fprintf(stderr, " %s %llu x %.0f", names[i], jp[i][1], (double)jp[i][0] / jp[i][1]);
     fprintf(stderr, "\n");
     std::memset(jp, 0, sizeof jp);

@@ -285,7 +285,7 @@ DEV void st_release(u32* p, u32 v) {
 
 // PBH_PROF diagnostics of the grid jobs (leader CTA, thread 0): cycles and
 // count per job kind [0, 8), and per phase of the bucket sort [8, 12).
-__device__ unsigned long long g_jobprof[16][2];
+__device__ unsigned long long g_jobprof[24][2];
 __device__ unsigned int g_jobprof_on;
 DEV void jobprof_add(u32 slot, long long cycles) {
   if (g_jobprof_on && threadIdx.x == 0 && blockIdx.x == 0) {
@@ -309,13 +309,20 @@ DEV u32 grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u3
   const bool filter = J.filter != 0;
   u32 ph = g.mph;
   u32 written = 0;
-  while (ia < ia_end || ib < ib_end) {
-    const u32 na = min(kGridTile, ia_end - ia), nb = min(kGridTile, ib_end - ib);
-    const u32 n = min(kGridTile, (ia_end - ia) + (ib_end - ib));
-    const Window<4> wak(J.ak, ia, na), wbk(J.bk, ib, nb);
-    const Window<8> wap(J.ap, ia, na), wbp(J.bp, ib, nb);
+  u32 na = 0, nb = 0, n = 0;
+  Window<4> wak, wbk;
+  Window<8> wap, wbp;
+  // the next tile's windows, and their TMA loads (thread 0, one mbarrier)
+  auto plan = [&]() {
+    na = min(kGridTile, ia_end - ia);
+    nb = min(kGridTile, ib_end - ib);
+    n = min(kGridTile, (ia_end - ia) + (ib_end - ib));
+    wak = Window<4>(J.ak, ia, na);
+    wbk = Window<4>(J.bk, ib, nb);
+    wap = Window<8>(J.ap, ia, na);
+    wbp = Window<8>(J.bp, ib, nb);
     if (tid == 0) {
-      fence_proxy_async_smem();  // the windows' previous readers are done (barrier above)
+      fence_proxy_async_smem();
       mbar_expect_tx(&g.mbar, (na ? wak.bytes + wap.bytes : 0u) + (nb ? wbk.bytes + wbp.bytes : 0u));
       if (na) {
         tma_load_1d(g.ak, wak.src, wak.bytes, &g.mbar);
@@ -326,8 +333,15 @@ DEV u32 grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u3
         tma_load_1d(g.bp, wbp.src, wbp.bytes, &g.mbar);
       }
     }
+  };
+  bool more = ia < ia_end || ib < ib_end;
+  if (more) plan();
+  long long tw = clock64();
+  while (more) {
     mbar_wait(&g.mbar, ph);
     ph ^= 1u;
+    jobprof_add(18, clock64() - tw);
+    tw = clock64();
     const u32* AK = g.ak + wak.off;
     const u64* AP = g.ap + wap.off;
     const u32* BK = g.bk + wbk.off;
@@ -358,6 +372,7 @@ DEV u32 grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u3
       }
     }
     if (d0 < d1 && d1 == n) g.ta = x;
+    u32 cnt = n;
     if (!filter) {
 #pragma unroll
       for (u32 v = 0; v < VT; ++v)
@@ -365,9 +380,6 @@ DEV u32 grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u3
           g.ok[d0 + v] = rk[v];
           g.op[d0 + v] = rp[v];
         }
-      Bk::sync();
-      for (u32 i = tid; i < n; i += NT) J.sink.put(out + i, g.ok[i], g.op[i]);
-      written += n;
     } else {
       // drop stale entries (primitives.cpp:103-120 semantics through the
       // position index): the survivors keep their merged order, compacted
@@ -376,8 +388,7 @@ DEV u32 grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u3
 #pragma unroll
       for (u32 v = 0; v < VT; ++v)
         if (d0 + v < d1 && entry_valid(J.idx, rk[v], rp[v])) keepm |= 1u << v;
-      u32 tot;
-      u32 pos = Bk::scan_excl(__popc(keepm), tot, g.scr);
+      u32 pos = Bk::scan_excl(__popc(keepm), cnt, g.scr);
 #pragma unroll
       for (u32 v = 0; v < VT; ++v)
         if (keepm >> v & 1u) {
@@ -385,15 +396,24 @@ DEV u32 grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u3
           g.op[pos] = rp[v];
           ++pos;
         }
-      Bk::sync();
-      for (u32 i = tid; i < tot; i += NT) J.sink.put(out + written + i, g.ok[i], g.op[i]);
-      written += tot;
     }
+    fence_proxy_async_smem();  // the window reads above, before the next TMA writes
+    Bk::sync();
+    jobprof_add(19, clock64() - tw);
+    tw = clock64();
+    // advance, and start the next tile's loads before storing this one
     const u32 ta = g.ta;
+    const u32 base = filter ? out + written : out;
     ia += ta;
     ib += n - ta;
     if (!filter) out += n;
+    more = ia < ia_end || ib < ib_end;
+    if (more) plan();
+    for (u32 i = tid; i < cnt; i += NT) J.sink.put(base + i, g.ok[i], g.op[i]);
+    written += cnt;
     Bk::sync();
+    jobprof_add(20, clock64() - tw);
+    tw = clock64();
   }
   if (tid == 0) g.mph = ph;
   return written;
@@ -841,9 +861,12 @@ DEV void grid_share(const GridJob& J, u32 b, GridSmem<NT>& g, u32* scratch) {
     return;
   }
   if (r0 >= r1) return;
+  long long tq = clock64();
   u32 a0, a1;
   merge_split2<NT>(A, B, r0, r1, scratch, a0, a1);
+  if (b == 0) { jobprof_add(16, clock64() - tq); tq = clock64(); }
   grid_stream<NT>(J, a0, a1, r0 - a0, r1 - a1, J.out_base + r0, g);
+  if (b == 0) jobprof_add(17, clock64() - tq);
 }
 
 // Helper CTAs: wait for jobs until the exit job.
