@@ -461,7 +461,9 @@ struct BankHeap {
     const u32 n = qn;
     if (n == 0) return;
     long long t = clock64();
-    if (bj && hc.gj && n >= kGridFlushMin && grid_flush_sort(n)) {
+    if (bj && hc.gj && n >= kGridFlushMin && grid_flush_merge(n, t)) {
+      // sorted and merged into S_1 by one grid job, resolves done
+    } else if (bj && hc.gj && n >= kGridFlushMin && grid_flush_sort(n)) {
       pr(8, t);
       push_run(bj->sk[1], bj->sp[1], n);
     } else {
@@ -475,6 +477,59 @@ struct BankHeap {
     if (tid == 0) L.qn = 0;
     qn = 0;
     Bk::sync();
+  }
+
+  // The push buffer merged into S_1 by ONE grid job (job 9: bucket by S_1
+  // chunks, sort each bucket, merge it with its chunk), then the 4-to-1
+  // resolve schedule. False (nothing changed) when the fused path does not
+  // apply: no level 1 yet, S_1 too small to bucket by or without room, a
+  // stale share that wants the filtered merge, or a bucket over the tile.
+  NOINL bool grid_flush_merge(u32 n, long long& t) {
+    if (hc.s.n_levels < 2) return false;
+    const pbh_level_state st1 = hc.s.st[1];
+    const u32 G = hc.gsz;
+    if (st1.s_size < 4 * G || (u64)st1.s_size + n > hc.s.lv[1].buf_s) return false;
+    to_cold();
+    if (hc.stale_share_above(kGridFilterNum, kGridFilterDen)) return false;
+    u32* const dk = bj->sk[0];
+    u64* const dp = bj->sp[0];
+    for (u32 i = tid; i < n; i += B) {
+      dk[i] = L.qk[i];
+      dp[i] = L.qp[i];
+    }
+    for (u32 i = tid; i < G; i += B) bj->bcnt[i] = 0;
+    const Run S1 = hc.signal(1);
+    const u32 ns = 1 - st1.s_sel;
+    if (tid == 0) {
+      bj->stg_n = n;
+      bj->mk = S1.k;
+      bj->mp = S1.p;
+      bj->mn = S1.n;
+      bj->ok = hc.s.lv[1].sk[ns];
+      bj->op = hc.s.lv[1].sp[ns];
+      bj->bovf = 0;
+    }
+    __threadfence();
+    Bk::sync();
+    grid_run<B>(hc.gj, G, 9, Run{}, Run{}, 0, Sink{}, 0, *hc.gs, hc.gs->scr);
+    if (*(volatile u32*)&bj->bovf) return false;
+    if (tid == 0) {
+      pbh_level_state& s1 = hc.s.st[1];
+      s1.s_sel = ns;
+      s1.s_head = 0;
+      s1.s_size = S1.n + n;
+      hc.s.touches[0] += 2ull * (S1.n + n);
+    }
+    Bk::sync();
+    pr(9, t);
+    ++pushes;
+    for (u32 i = 1; i < hc.s.n_levels && i < 31 && !hc.failed(); ++i) {
+      if (pushes & ((1ull << (2 * i)) - 1)) break;  // resolve(i) every 4^i pushes
+      hc.resolve(i);
+      pr(9 + (i < 6 ? i : 6), t);
+    }
+    after_cold();
+    return true;
   }
 
   // The push buffer sorted by the whole grid: staged to HBM (bj->sk/sp[0])

@@ -599,7 +599,7 @@ void prof_report(pbh_heap* h, const char* when) {
   if (cudaMemcpyFromSymbol(jp, g_jobprof, sizeof jp) == cudaSuccess) {
     static const char* names[24] = {"merge", "exit", "validate", "classify", "chunks", "pass",
                                     "check+classify", "bucket_sort", "b:hist", "b:bar1", "b:scatter",
-                                    "b:bar2", "b:sort", "leader_wait", "filtered_merge", "-",
+                                    "b:bar2", "b:sort", "leader_wait", "filtered_merge", "flush_merge",
                                     "m:split", "m:stream", "s:tma_wait", "s:merge", "s:store", "-", "-", "-"};
     fprintf(stderr, "pbh_jobprof[%s]:", when);
     for (int i = 0; i < 24; ++i)

@@ -187,7 +187,8 @@ struct GridJob {
   u32 kind;  // 0 = merge, 1 = exit, 2 = validate batch, 3 = classify batch,
              // 4 = sort chunks, 5 = merge pass, 6 = validate + classify (no
              // mutation), 7 = bucket sort of the staged run (BatchJob in `ext`),
-             // 8 = merge dropping stale entries (compacting; count in ext)
+             // 8 = merge dropping stale entries (compacting; count in ext),
+             // 9 = merge an unsorted run into a sorted one (push-buffer flush)
   u32 nblk;  // CTAs in the grid (leader included)
   const u32* ak;
   const u64* ap;
@@ -238,6 +239,13 @@ struct BatchJob {
   u32* bcnt;      // per-bucket element counts (kBucketMax)
   u32 nbkt, bovf; // bucket count; set when a bucket exceeds kGridTile
   u32 merge_total;  // kind 8: entries written
+  // kind 9: the unsorted run sk/sp[0][0, stg_n) merged with the sorted run
+  // (mk, mp)[0, mn) into (ok, op)
+  const u32* mk;
+  const u64* mp;
+  u32 mn, pad9_;
+  u32* ok;
+  u64* op;
 };
 constexpr u32 kBucketMax = 1184;  // 8 buckets per CTA of a 148-CTA grid
 constexpr u32 kRankSortMax = 192;  // buckets up to this size: rank sort (measured vs cta_sort)
@@ -814,6 +822,143 @@ DEV void batch_bucket_sort(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
   if (b == 0) jobprof_add(12, clock64() - tp);
 }
 
+// Sort m entries (DK, DP)[s0, s0 + m) in place in the CTA: rank sort for
+// small runs ((p, k) pairs are unique), else the CTA merge sort in the
+// windows (m <= kGridTile).
+template <int NT>
+DEV void cta_sort_hbm(u32* DK, u64* DP, u32 s0, u32 m, GridSmem<NT>& g) {
+  using Bk = Blk<NT>;
+  if (m < 2) return;
+  if (m <= kRankSortMax) {
+    u32 k0 = 0;
+    u64 p0 = 0;
+    const u32 i0 = threadIdx.x;
+    if (i0 < m) {
+      k0 = DK[s0 + i0];
+      p0 = DP[s0 + i0];
+      g.ak[i0] = k0;
+      g.ap[i0] = p0;
+    }
+    Bk::sync();
+    u32 r0 = 0;
+    for (u32 j = 0; j < m; ++j) r0 += less_pk(g.ap[j], g.ak[j], p0, k0);
+    if (i0 < m) {
+      DK[s0 + r0] = k0;
+      DP[s0 + r0] = p0;
+    }
+    Bk::sync();
+    return;
+  }
+  for (u32 i = threadIdx.x; i < m; i += NT) {
+    g.ak[i] = DK[s0 + i];
+    g.ap[i] = DP[s0 + i];
+  }
+  Bk::sync();
+  cta_sort<NT / 32>(g.ak, g.ap, m, g.bk, g.bp);
+  for (u32 i = threadIdx.x; i < m; i += NT) {
+    DK[s0 + i] = g.ak[i];
+    DP[s0 + i] = g.ap[i];
+  }
+  Bk::sync();
+}
+
+// kind 9: merge the unsorted run U = sk/sp[0][0, n) into the sorted run
+// S = (mk, mp)[0, m), into (ok, op)[0, m + n), in one job. CTA b owns the S
+// chunk [m·b/G, m·(b+1)/G) and the U entries between its chunk's first
+// entry and the next chunk's (bucket b): (1) every CTA holds the G - 1 chunk
+// heads; each buckets its slice of U (binary search), with global bucket
+// bases; (2) after a barrier, scatter U into bucket order (sk/sp[1]); (3)
+// after a second barrier, CTA b sorts its bucket in place and streams the
+// merge of its S chunk with it to output position m·b/G + (U entries in
+// earlier buckets). A bucket above kGridTile sets bovf (the leader then
+// takes the two-job path; S and U are untouched).
+template <int NT>
+DEV void batch_flush_merge(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
+  using Bk = Blk<NT>;
+  const u32 n = X->stg_n, m = X->mn;
+  const u32* MK = X->mk;
+  const u64* MP = X->mp;
+  const u32* UK = X->sk[0];
+  const u64* UP = X->sp[0];
+  u32* DK = X->sk[1];
+  u64* DP = X->sp[1];
+  // chunk heads 1..G-1 in the output windows (ok / op), counters in ap
+  u32* hk = g.ok;
+  u64* hp = g.op;
+  u32* cnt = reinterpret_cast<u32*>(g.ap);
+  u32* base = cnt + kBucketMax;
+  u32* start = base + kBucketMax;
+  for (u32 i = threadIdx.x; i < G; i += NT) {
+    cnt[i] = 0;
+    if (i >= 1) {
+      const u32 at = (u32)((u64)m * i / G);
+      const bool ok = at < m;  // empty tail chunks sort after everything
+      hk[i - 1] = ok ? MK[at] : 0xffffffffu;
+      hp[i - 1] = ok ? MP[at] : ~0ull;
+    }
+  }
+  Bk::sync();
+  auto bucket_of = [&](u32 k, u64 p) {  // heads <= (p, k), i.e. upper bound
+    u32 lo = 0, hi = G - 1;
+    while (lo < hi) {
+      const u32 mid = (lo + hi) >> 1;
+      if (!less_pk(p, k, hp[mid], hk[mid]))
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    return lo;
+  };
+  const u32 r0 = (u32)((u64)n * b / G), r1 = (u32)((u64)n * (b + 1) / G);
+  for (u32 j = r0 + threadIdx.x; j < r1; j += NT) atomicAdd(&cnt[bucket_of(UK[j], UP[j])], 1u);
+  Bk::sync();
+  for (u32 i = threadIdx.x; i < G; i += NT) {
+    const u32 c = cnt[i];
+    base[i] = c ? atomicAdd(&X->bcnt[i], c) : 0;
+    cnt[i] = 0;
+  }
+  job_barrier<NT>(X, G, g);
+  {
+    u32 run = 0;
+    for (u32 i0 = 0; i0 < G; i0 += NT) {
+      const u32 i = i0 + threadIdx.x;
+      const u32 v = i < G ? __ldcg(&X->bcnt[i]) : 0;
+      u32 tot;
+      const u32 e = run + Bk::scan_excl(v, tot, g.scr);
+      if (i < G) start[i] = e;
+      run += tot;
+    }
+  }
+  Bk::sync();
+  for (u32 j = r0 + threadIdx.x; j < r1; j += NT) {
+    const u32 k = UK[j];
+    const u64 p = UP[j];
+    const u32 q = bucket_of(k, p);
+    const u32 pos = start[q] + base[q] + atomicAdd(&cnt[q], 1u);
+    DK[pos] = k;
+    DP[pos] = p;
+  }
+  job_barrier<NT>(X, G, g);
+  const u32 ub = __ldcg(&X->bcnt[b]), us = start[b];
+  if (ub > kGridTile) {
+    if (threadIdx.x == 0) atomicOr(&X->bovf, 1u);
+    return;
+  }
+  cta_sort_hbm<NT>(DK, DP, us, ub, g);
+  const u32 m0 = (u32)((u64)m * b / G), m1 = (u32)((u64)m * (b + 1) / G);
+  if (threadIdx.x == 0) {
+    g.sub.ak = MK + m0;
+    g.sub.ap = MP + m0;
+    g.sub.bk = DK + us;
+    g.sub.bp = DP + us;
+    g.sub.sink = Sink{X->ok, X->op, 0xffffffffu, nullptr, nullptr};
+    g.sub.filter = 0;
+  }
+  __threadfence_block();
+  Bk::sync();
+  grid_stream<NT>(g.sub, 0, m1 - m0, 0, ub, m0 + us, g);
+}
+
 // This CTA's share (block b of G) of the current job.
 template <int NT>
 DEV void grid_share(const GridJob& J, u32 b, GridSmem<NT>& g, u32* scratch) {
@@ -825,6 +970,7 @@ DEV void grid_share(const GridJob& J, u32 b, GridSmem<NT>& g, u32* scratch) {
     case 5: return batch_merge_pass<NT>(J.ext, b, G, g, scratch);
     case 6: return batch_check_classify<NT>(J.ext, b, G, g);
     case 7: return batch_bucket_sort<NT>(J.ext, b, G, g);
+    case 9: return batch_flush_merge<NT>(J.ext, b, G, g);
     default: break;
   }
   const u32 r0 = (u32)((u64)J.c * b / G), r1 = (u32)((u64)J.c * (b + 1) / G);
@@ -972,7 +1118,7 @@ NOINL void grid_run(GridJob* gj, u32 G, u32 kind, const Run& A, const Run& B, u3
     __threadfence();
   }
   Bk::sync();
-  jobprof_add(kind == 8 ? 14u : kind, clock64() - t_job);
+  jobprof_add(kind == 8 ? 14u : kind == 9 ? 15u : kind, clock64() - t_job);
   jobprof_add(13, clock64() - t_share);  // leader waiting for the helpers
 }
 
