@@ -485,18 +485,34 @@ struct BankHeap {
   // apply: no level 1 yet, S_1 too small to bucket by or without room, a
   // stale share that wants the filtered merge, or a bucket over the tile.
   NOINL bool grid_flush_merge(u32 n, long long& t) {
-    if (hc.s.n_levels < 2) return false;
-    const pbh_level_state st1 = hc.s.st[1];
-    const u32 G = hc.gsz;
-    if (st1.s_size < 4 * G || (u64)st1.s_size + n > hc.s.lv[1].buf_s) return false;
-    to_cold();
-    if (hc.stale_share_above(kGridFilterNum, kGridFilterDen)) return false;
+    if (!grid_push_fits(n)) return false;
     u32* const dk = bj->sk[0];
     u64* const dp = bj->sp[0];
     for (u32 i = tid; i < n; i += B) {
       dk[i] = L.qk[i];
       dp[i] = L.qp[i];
     }
+    return grid_push_unsorted(n, false, t);
+  }
+
+  // Whether job 9 can take a push of n entries into S_1 now (level 1
+  // exists, S_1 is large enough to bucket by and has room, and no filtered
+  // merge is due). Writes the level-0 state to the cold engine.
+  NOINL bool grid_push_fits(u32 n) {
+    if (hc.s.n_levels < 2) return false;
+    const pbh_level_state& st1 = hc.s.st[1];
+    if (st1.s_size < 4 * hc.gsz || (u64)st1.s_size + n > hc.s.lv[1].buf_s) return false;
+    to_cold();
+    return !hc.stale_share_above(kGridFilterNum, kGridFilterDen);
+  }
+
+  // Job 9 over the unsorted run staged in bj->sk/sp[0][0, n), then the
+  // 4-to-1 resolve schedule (push_run's tail). write_idx: publish each
+  // entry's index entry {p, LIVE, deep} (a staged big batch). False when a
+  // bucket overflowed (S_1 unchanged; the caller sorts and pushes).
+  NOINL bool grid_push_unsorted(u32 n, bool write_idx, long long& t) {
+    const pbh_level_state st1 = hc.s.st[1];
+    const u32 G = hc.gsz;
     for (u32 i = tid; i < G; i += B) bj->bcnt[i] = 0;
     const Run S1 = hc.signal(1);
     const u32 ns = 1 - st1.s_sel;
@@ -508,6 +524,7 @@ struct BankHeap {
       bj->ok = hc.s.lv[1].sk[ns];
       bj->op = hc.s.lv[1].sp[ns];
       bj->bovf = 0;
+      bj->write_idx = write_idx ? 1u : 0u;
     }
     __threadfence();
     Bk::sync();
@@ -1448,7 +1465,18 @@ __global__ void __launch_bounds__(32 * NW, 1)
         live += *(volatile u32*)&bj->fresh;
         lst = bj->ll;
         TPROF(6);
+        bool big_pushed = false;
         if (stg_n) {
+          // the staged part straight into S_1 (job 9: bucket by S_1 chunks,
+          // sort, merge, publish the index entries) when S_1 allows it
+          BANK_TO_H();
+          long long tj = clock64();
+          if (H.grid_push_fits(stg_n) && H.grid_push_unsorted(stg_n, true, tj)) big_pushed = true;
+          BANK_FROM_H();
+          if (hc.failed()) break;
+          TPROF(8 - 1);
+        }
+        if (stg_n && !big_pushed) {
           // the HBM-bound part of the batch, sorted by (p, k) on the grid:
           // a bucket sort (one job) when the buckets fit the CTA tiles,
           // else CTA-sorted chunks + merge passes; both publish the staged

@@ -882,6 +882,8 @@ DEV void batch_flush_merge(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
   const u64* UP = X->sp[0];
   u32* DK = X->sk[1];
   u64* DP = X->sp[1];
+  const bool write_idx = X->write_idx;
+  pbh_idx_entry* idx = X->idx;
   // chunk heads 1..G-1 in the output windows (ok / op), counters in ap
   u32* hk = g.ok;
   u64* hp = g.op;
@@ -937,6 +939,13 @@ DEV void batch_flush_merge(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
     const u32 pos = start[q] + base[q] + atomicAdd(&cnt[q], 1u);
     DK[pos] = k;
     DP[pos] = p;
+    if (write_idx) {
+      pbh_idx_entry ne;
+      ne.prio = p;
+      ne.state = PBH_ST_LIVE | (PBH_LOC_DEEP << 2);
+      ne.parent = 0;
+      reinterpret_cast<ulonglong2*>(idx)[k] = *reinterpret_cast<const ulonglong2*>(&ne);
+    }
   }
   job_barrier<NT>(X, G, g);
   const u32 ub = __ldcg(&X->bcnt[b]), us = start[b];
