@@ -85,10 +85,13 @@ struct BankSmem {
   static constexpr int B = 32 * NW;
   static constexpr int C0 = B * KI;
   BankL0<B, KI, MW> l0;
-  // cold-engine B_0 ping-pong (capacity C0/2 each); as one C0-entry array
-  // it is also the sort scratch of evict()
-  u32 bk[2][C0 / 2];
-  u64 bp[2][C0 / 2];
+  // cold-engine B_0 ping-pong; as one array (>= C0 entries) it is also the
+  // sort scratch of evict(). A refill pulls up to its capacity: C0/2, or
+  // 3/4 of C0 for the threshold engine (its batches drain level 0 fast;
+  // fewer, larger refills)
+  static constexpr int B0CAP = MW ? (C0 * 3) / 4 : C0 / 2;
+  u32 bk[2][B0CAP];
+  u64 bp[2][B0CAP];
   u32 sk[kBankQ];  // sort scratch of the push-buffer flush
   u64 sp[kBankQ];
   u32 pf_t[kBankPass];  // next row's first pass, prefetched by cp.async

@@ -126,6 +126,9 @@ struct BankCfg<4> { static constexpr int KI = 8; };
 template <>
 struct BankCfg<8> { static constexpr int KI = 4; };
 constexpr int kBankC0 = 1024;
+constexpr u32 kMultiCap0 = kBankC0 * 3 / 4;  // threshold engine's B_0 (BankSmem<..., true>::B0CAP)
+static_assert(kMultiCap0 == (u32)BankSmem<4, 8, VT, true>::B0CAP, "threshold B_0 capacity");
+static_assert(kBankC0 / 2 == BankSmem<4, 8, VT, false>::B0CAP, "exact B_0 capacity");
 
 template <int NW>
 size_t bank_save_bytes() {
@@ -1260,12 +1263,14 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
     base1 = std::max<u64>(strtoull(e, nullptr, 10), 2ull * kBankQ);
     nlev = 2;
   }
+  // level 0 is allocated for the threshold engine's larger refills
+  // (kMultiCap0); exact mode refills to kBankC0 / 2 (c->cap0)
   size_t per_heap = 0;
   {
     DevHeap M;
     M.measure = true;
     M.base1 = base1, M.bank = true;
-    init_heap(M, c->d, c->cap0, bc, c->nt, std::max<u32>(c->V, 1), 0, nlev, c->d_heaps);
+    init_heap(M, c->d, kMultiCap0, bc, c->nt, std::max<u32>(c->V, 1), 0, nlev, c->d_heaps);
     per_heap = M.measured;
   }
   char* arena = nullptr;
@@ -1275,9 +1280,10 @@ pbh_status pbh_sssp_ctx_create(const pbh_csr* g, uint64_t d, int device, uint64_
     H.base1 = base1, H.bank = true;
     H.arena = arena + per_heap * i;
     H.arena_cap = per_heap;
-    st = init_heap(H, c->d, c->cap0, bc, c->nt, std::max<u32>(c->V, 1), 0, nlev, c->d_heaps + i,
+    st = init_heap(H, c->d, kMultiCap0, bc, c->nt, std::max<u32>(c->V, 1), 0, nlev, c->d_heaps + i,
                    c->stream);
     if (st) return fail(st);
+    H.hd.cap0 = c->cap0;  // uploaded with the header by every ctx_reset
   }
   CK(cudaStreamSynchronize(c->stream));
   *out = c;
@@ -1421,6 +1427,8 @@ pbh_status pbh_sssp_ctx_set_mode(pbh_sssp_ctx* c, int mode) {
     CK(cudaStreamSynchronize(c->stream));
   }
   c->multi = mode == 1;
+  c->cap0 = c->multi ? kMultiCap0 : kBankC0 / 2;
+  for (auto& H : c->heaps) H.hd.cap0 = c->cap0;
   return PBH_OK;
 }
 
