@@ -302,6 +302,19 @@ DEV void tma_load_1d(void* dst, const void* src, u32 bytes, u64* bar) {
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Bulk store of `bytes` (multiple of 16, both addresses 16-byte aligned)
+// from this CTA's shared memory to global memory, in the thread's bulk group.
+DEV void tma_store_1d(void* dst, const void* src, u32 bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+// The committed bulk stores have read their shared-memory sources.
+DEV void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+// The committed bulk stores are complete (their writes visible).
+DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
 // A 16-byte aligned window covering elements [i, i + n) of an array of
 // E-byte elements: source address, element offset of i inside the window,
 // and the copy size.

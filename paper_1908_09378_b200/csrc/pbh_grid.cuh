@@ -257,10 +257,10 @@ struct GridSmem {
   // alignment offset of a window start) and the output tile
   alignas(16) u32 ak[kGridTile + 4];
   alignas(16) u32 bk[kGridTile + 4];
-  alignas(16) u32 ok[kGridTile];
+  alignas(16) u32 ok[kGridTile + 4];
   alignas(16) u64 ap[kGridTile + 2];
   alignas(16) u64 bp[kGridTile + 2];
-  alignas(16) u64 op[kGridTile];
+  alignas(16) u64 op[kGridTile + 2];
   GridJob job;  // the current job, copied in by thread 0
   u64 mbar;     // window-load barrier (one phase per tile)
   u32 mph;      // its next phase parity
@@ -380,13 +380,30 @@ DEV u32 grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u3
       }
     }
     if (d0 < d1 && d1 == n) g.ta = x;
+    // where this tile's outputs land: one destination run (bulk-stored from
+    // a staging tile shifted to the destination's 16-byte phase) unless the
+    // tile straddles the sink's split point (element stores)
+    const u32 base = filter ? out + written : out;
+    u32* dk = nullptr;
+    u64* dp = nullptr;
+    if (base + n <= J.sink.lim) {
+      dk = J.sink.k1 + base;
+      dp = J.sink.p1 + base;
+    } else if (base >= J.sink.lim) {
+      dk = J.sink.k2 + (base - J.sink.lim);
+      dp = J.sink.p2 + (base - J.sink.lim);
+    }
+    const u32 shk = dk ? (u32)((reinterpret_cast<uintptr_t>(dk) >> 2) & 3u) : 0u;
+    const u32 shp = dp ? (u32)((reinterpret_cast<uintptr_t>(dp) >> 3) & 1u) : 0u;
+    if (tid == 0) bulk_wait_read();  // the previous tile's bulk stores left the staging tile
+    Bk::sync();
     u32 cnt = n;
     if (!filter) {
 #pragma unroll
       for (u32 v = 0; v < VT; ++v)
         if (d0 + v < d1) {
-          g.ok[d0 + v] = rk[v];
-          g.op[d0 + v] = rp[v];
+          g.ok[shk + d0 + v] = rk[v];
+          g.op[shp + d0 + v] = rp[v];
         }
     } else {
       // drop stale entries (primitives.cpp:103-120 semantics through the
@@ -400,30 +417,50 @@ DEV u32 grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u3
 #pragma unroll
       for (u32 v = 0; v < VT; ++v)
         if (keepm >> v & 1u) {
-          g.ok[pos] = rk[v];
-          g.op[pos] = rp[v];
+          g.ok[shk + pos] = rk[v];
+          g.op[shp + pos] = rp[v];
           ++pos;
         }
     }
-    fence_proxy_async_smem();  // the window reads above, before the next TMA writes
+    fence_proxy_async_smem();  // window reads and staging writes vs. the async proxy
     Bk::sync();
     jobprof_add(19, clock64() - tw);
     tw = clock64();
     // advance, and start the next tile's loads before storing this one
     const u32 ta = g.ta;
-    const u32 base = filter ? out + written : out;
     ia += ta;
     ib += n - ta;
     if (!filter) out += n;
     more = ia < ia_end || ib < ib_end;
     if (more) plan();
-    for (u32 i = tid; i < cnt; i += NT) J.sink.put(base + i, g.ok[i], g.op[i]);
+    if (dk) {
+      // aligned middles by two bulk stores (thread 0), the unaligned head
+      // and tail entries by threads
+      const u32 k0 = (shk + 3u) & ~3u, k1 = (shk + cnt) & ~3u;  // staging indices
+      const u32 p0 = (shp + 1u) & ~1u, p1 = (shp + cnt) & ~1u;
+      const bool kb = k1 > k0, pb = p1 > p0;
+      if (tid == 0) {
+        if (kb) tma_store_1d(dk + (k0 - shk), g.ok + k0, (k1 - k0) * 4);
+        if (pb) tma_store_1d(dp + (p0 - shp), g.op + p0, (p1 - p0) * 8);
+        if (kb || pb) bulk_commit();
+      }
+      for (u32 i = tid; i < cnt; i += NT) {
+        const u32 sk = shk + i, sp = shp + i;
+        if (!kb || sk < k0 || sk >= k1) dk[i] = g.ok[sk];
+        if (!pb || sp < p0 || sp >= p1) dp[i] = g.op[sp];
+      }
+    } else {
+      for (u32 i = tid; i < cnt; i += NT) J.sink.put(base + i, g.ok[i], g.op[i]);
+    }
     written += cnt;
-    Bk::sync();
     jobprof_add(20, clock64() - tw);
     tw = clock64();
   }
-  if (tid == 0) g.mph = ph;
+  if (tid == 0) {
+    bulk_wait_all();  // the bulk stores' writes are complete before the job ends
+    g.mph = ph;
+  }
+  Bk::sync();
   return written;
 }
 
