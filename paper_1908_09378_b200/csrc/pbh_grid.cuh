@@ -249,6 +249,7 @@ struct BatchJob {
 };
 constexpr u32 kBucketMax = 1184;  // 8 buckets per CTA of a 148-CTA grid
 constexpr u32 kRankSortMax = 192;  // buckets up to this size: rank sort (measured vs cta_sort)
+constexpr u32 kBulkStoreMin = 1024;  // merge tiles at least this large leave by bulk stores
 
 template <int NT>
 struct GridSmem {
@@ -318,6 +319,7 @@ DEV u32 grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u3
   u32 ph = g.mph;
   u32 written = 0;
   u32 na = 0, nb = 0, n = 0;
+  bool bulk_pending = false;  // this CTA's bulk stores may still read the staging tile
   Window<4> wak, wbk;
   Window<8> wap, wbp;
   // the next tile's windows, and their TMA loads (thread 0, one mbarrier)
@@ -384,19 +386,26 @@ DEV u32 grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u3
     // a staging tile shifted to the destination's 16-byte phase) unless the
     // tile straddles the sink's split point (element stores)
     const u32 base = filter ? out + written : out;
+    // (small tiles: element stores; the bulk path's wait and barrier cost
+    // more than it saves below ~1024 entries, measured on C1 / C4 d=1024)
     u32* dk = nullptr;
     u64* dp = nullptr;
-    if (base + n <= J.sink.lim) {
-      dk = J.sink.k1 + base;
-      dp = J.sink.p1 + base;
-    } else if (base >= J.sink.lim) {
-      dk = J.sink.k2 + (base - J.sink.lim);
-      dp = J.sink.p2 + (base - J.sink.lim);
+    if (n >= kBulkStoreMin) {
+      if (base + n <= J.sink.lim) {
+        dk = J.sink.k1 + base;
+        dp = J.sink.p1 + base;
+      } else if (base >= J.sink.lim) {
+        dk = J.sink.k2 + (base - J.sink.lim);
+        dp = J.sink.p2 + (base - J.sink.lim);
+      }
     }
     const u32 shk = dk ? (u32)((reinterpret_cast<uintptr_t>(dk) >> 2) & 3u) : 0u;
     const u32 shp = dp ? (u32)((reinterpret_cast<uintptr_t>(dp) >> 3) & 1u) : 0u;
-    if (tid == 0) bulk_wait_read();  // the previous tile's bulk stores left the staging tile
-    Bk::sync();
+    if (bulk_pending) {  // the previous tile's bulk stores must have left the staging tile
+      if (tid == 0) bulk_wait_read();
+      Bk::sync();
+      bulk_pending = false;
+    }
     u32 cnt = n;
     if (!filter) {
 #pragma unroll
@@ -444,10 +453,23 @@ DEV u32 grid_stream(const GridJob& J, u32 ia, u32 ia_end, u32 ib, u32 ib_end, u3
         if (pb) tma_store_1d(dp + (p0 - shp), g.op + p0, (p1 - p0) * 8);
         if (kb || pb) bulk_commit();
       }
-      for (u32 i = tid; i < cnt; i += NT) {
-        const u32 sk = shk + i, sp = shp + i;
-        if (!kb || sk < k0 || sk >= k1) dk[i] = g.ok[sk];
-        if (!pb || sp < p0 || sp >= p1) dp[i] = g.op[sp];
+      bulk_pending = kb || pb;
+      if (kb && pb) {
+        // at most 3 + 3 key and 1 + 1 priority entries outside the middles
+        if (tid < 3) {
+          const u32 h = tid, t = k1 - shk + tid;  // head / tail output index
+          if (h < min(cnt, k0 - shk)) dk[h] = g.ok[shk + h];
+          if (t < cnt) dk[t] = g.ok[shk + t];
+        } else if (tid == (NT > 32 ? 32u : 3u)) {
+          if (shp < p0 && cnt) dp[0] = g.op[shp];
+          if (p1 - shp < cnt) dp[cnt - 1] = g.op[shp + cnt - 1];
+        }
+      } else {
+        for (u32 i = tid; i < cnt; i += NT) {
+          const u32 sk = shk + i, sp = shp + i;
+          if (!kb || sk < k0 || sk >= k1) dk[i] = g.ok[sk];
+          if (!pb || sp < p0 || sp >= p1) dp[i] = g.op[sp];
+        }
       }
     } else {
       for (u32 i = tid; i < cnt; i += NT) J.sink.put(base + i, g.ok[i], g.op[i]);
