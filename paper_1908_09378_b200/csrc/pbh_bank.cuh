@@ -464,7 +464,8 @@ struct BankHeap {
     const u32 n = qn;
     if (n == 0) return;
     long long t = clock64();
-    if (bj && hc.gj && n >= kGridFlushMin && grid_flush_merge(n, t)) {
+    if (bj && hc.gj && n >= kGridFlushMin &&
+        (grid_flush_merge(n, t) || grid_flush_union(n, t))) {
       // sorted and merged into S_1 by one grid job, resolves done
     } else if (bj && hc.gj && n >= kGridFlushMin && grid_flush_sort(n)) {
       pr(8, t);
@@ -556,7 +557,42 @@ struct BankHeap {
   // with its priority range, bucket-sorted into bj->sk/sp[1] (grid job 7,
   // index untouched). False when a bucket overflowed (the caller sorts in
   // the CTA; the push buffer is still intact).
-  NOINL bool grid_flush_sort(u32 n) {
+  NOINL bool grid_flush_sort(u32 n) { return grid_flush_bucket(n, nullptr); }
+
+  // S_1 too small for job 9 to bucket by: the push buffer and S_1 sorted
+  // together by job 7 straight into S_1's other buffer (no merge job), then
+  // the resolve schedule. False (nothing changed) when it does not apply.
+  NOINL bool grid_flush_union(u32 n, long long& t) {
+    if (hc.s.n_levels < 2) return false;
+    const pbh_level_state st1 = hc.s.st[1];
+    if (st1.s_size >= 4 * hc.gsz || (u64)st1.s_size + n > hc.s.lv[1].buf_s) return false;
+    to_cold();
+    if (hc.stale_share_above(kGridFilterNum, kGridFilterDen)) return false;
+    const Run S1 = hc.signal(1);
+    const u32 ns = 1 - st1.s_sel;
+    if (!grid_flush_bucket(n, &S1, hc.s.lv[1].sk[ns], hc.s.lv[1].sp[ns])) return false;
+    if (tid == 0) {
+      pbh_level_state& s1 = hc.s.st[1];
+      s1.s_sel = ns;
+      s1.s_head = 0;
+      s1.s_size = S1.n + n;
+      hc.s.touches[0] += 2ull * (S1.n + n);
+    }
+    Bk::sync();
+    pr(9, t);
+    ++pushes;
+    for (u32 i = 1; i < hc.s.n_levels && i < 31 && !hc.failed(); ++i) {
+      if (pushes & ((1ull << (2 * i)) - 1)) break;  // resolve(i) every 4^i pushes
+      hc.resolve(i);
+      pr(9 + (i < 6 ? i : 6), t);
+    }
+    after_cold();
+    return true;
+  }
+
+  // Job 7 over the push buffer (plus, when `also`, a sorted run folded in),
+  // into bj->sk/sp[1] or, when given, (ok, op).
+  NOINL bool grid_flush_bucket(u32 n, const Run* also, u32* ok = nullptr, u64* op = nullptr) {
     u64 lo = ~0ull, hi = 0;
     u32* const dk = bj->sk[0];
     u64* const dp = bj->sp[0];
@@ -564,6 +600,14 @@ struct BankHeap {
       const u64 p = L.qp[i];
       dk[i] = L.qk[i];
       dp[i] = p;
+      lo = min(lo, p);
+      hi = max(hi, p);
+    }
+    const u32 m = also ? also->n : 0u;
+    for (u32 i = tid; i < m; i += B) {
+      const u64 p = also->p[i];
+      dk[n + i] = also->k[i];
+      dp[n + i] = p;
       lo = min(lo, p);
       hi = max(hi, p);
     }
@@ -586,13 +630,15 @@ struct BankHeap {
       const u64 range = b - a;
       u32 nb = G;
       if (range < (u64)nb - 1) nb = (u32)range + 1;
-      bj->stg_n = n;
+      bj->stg_n = n + m;
       bj->pmin = a;
       bj->pmax = b;
       bj->nbkt = nb;
       bj->bwidth = range / nb + 1;
       bj->bovf = 0;
       bj->write_idx = 0;
+      bj->ok = ok;
+      bj->op = op;
       S.fr_nb = nb;
     }
     Bk::sync();
@@ -1497,6 +1543,8 @@ __global__ void __launch_bounds__(32 * NW, 1)
               bj->bwidth = range / nb + 1;
               bj->bovf = 0;
               bj->write_idx = 1;
+              bj->ok = nullptr;
+              bj->op = nullptr;
             }
             __threadfence();
             Bk::sync();

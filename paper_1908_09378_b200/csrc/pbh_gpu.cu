@@ -712,7 +712,8 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
   if (h->d_job) {
     // grid sorts: job block + staging / sort ping-pong / leader list, for
     // large batches (d >= kBigBatch) and the push-buffer flushes (kBankQ)
-    const u64 cap = std::max<u64>(std::min<u64>(d, kMaxBatch), kBankQ);
+    // (+ room for a small S_1 folded into a push-buffer flush sort)
+    const u64 cap = std::max<u64>(std::min<u64>(d, kMaxBatch), 2 * kBankQ);
     BatchJob hb{};
     void* mem[6] = {};
     void* bc = nullptr;
@@ -735,6 +736,10 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
     hb.stg_p = hb.sp[0];
     if (cudaMemcpy(h->d_batch, &hb, sizeof hb, cudaMemcpyHostToDevice) != cudaSuccess)
       return fail(set_err(PBH_CUDA, "batch job init"));
+  }
+  if (getenv("PBH_AB_OFF")) {
+    const unsigned int on = 1;
+    cudaMemcpyToSymbol(g_ab_off, &on, sizeof on);
   }
   if (getenv("PBH_PROF") && cudaMalloc(&h->d_prof, 16 * sizeof(unsigned long long)) == cudaSuccess) {
     cudaMemset(h->d_prof, 0, 16 * sizeof(unsigned long long));

@@ -797,8 +797,9 @@ DEV void batch_bucket_sort(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
     }
   }
   Bk::sync();
-  u32* DK = X->sk[1];
-  u64* DP = X->sp[1];
+  // output: the sorted-run buffer, or (ok, op) when the caller gave one
+  u32* DK = X->ok ? X->ok : X->sk[1];
+  u64* DP = X->ok ? X->op : X->sp[1];
   const bool write_idx = X->write_idx;
   pbh_idx_entry* idx = X->idx;
   for (u32 j = r0 + threadIdx.x; j < r1; j += NT) {

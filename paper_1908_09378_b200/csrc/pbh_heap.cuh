@@ -12,8 +12,8 @@ constexpr u32 kInfCount = 0xffffffffu;
 // Stale shares of the deep content above which the grid (two gather passes)
 // and the streamed (one pass) merges drop stale entries (measured: below
 // them the gathers cost more than the carried entries, C1 and C4).
-constexpr u32 kGridFilterNum = 3, kGridFilterDen = 4;
-constexpr u32 kStreamFilterNum = 3, kStreamFilterDen = 4;
+constexpr u32 kGridFilterNum = 7, kGridFilterDen = 8;
+constexpr u32 kStreamFilterNum = 7, kStreamFilterDen = 8;
 
 template <int NT, int VT>
 struct HeapSmem {
@@ -101,6 +101,7 @@ struct HeapCta {
     return out;
   }
   DEV bool stale_share_above(u32 num, u32 den) const {
+    if (g_ab_off) return false;
     const u64 stored = content_from(1);
     const u64 lv = s.live > 0 ? (u64)s.live : 0ull;
     const u64 stale = stored > lv ? stored - lv : 0ull;

@@ -1,0 +1,11 @@
+for r in 1 2 3; do
+  for v in on off; do
+    if [ $v = off ]; then export PBH_AB_OFF=1; else unset PBH_AB_OFF; fi
+    timeout 300 python tools/probe_c4.py --ds 1024,65536 --c1 20000 2>&1 | grep cfg | python -c "
+import sys, json
+out=[]
+for l in sys.stdin:
+    d=json.loads(l); out.append('%s=%.3f' % (d['cfg']+str(d.get('d','')), d.get('us_per_batch', d.get('us_per_op', 0))))
+print('$v', ' '.join(out))"
+  done
+done
