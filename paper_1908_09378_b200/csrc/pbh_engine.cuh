@@ -45,8 +45,6 @@ using i64 = int64_t;
 
 DEV bool less_pk(u64 pa, u32 ka, u64 pb, u32 kb) { return pa < pb || (pa == pb && ka < kb); }
 
-__device__ unsigned int g_ab_off;  // A/B experiment switch (development; PBH_AB_OFF)
-
 // Splitter::admits (element.hpp:55-59): key <= splitter, infinity admits all.
 DEV bool admits(const pbh_level_state& s, u64 p, u32 k) {
   return s.spl_inf || p < s.spl_p || (p == s.spl_p && k <= s.spl_k);

@@ -737,10 +737,6 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
     if (cudaMemcpy(h->d_batch, &hb, sizeof hb, cudaMemcpyHostToDevice) != cudaSuccess)
       return fail(set_err(PBH_CUDA, "batch job init"));
   }
-  if (getenv("PBH_AB_OFF")) {
-    const unsigned int on = 1;
-    cudaMemcpyToSymbol(g_ab_off, &on, sizeof on);
-  }
   if (getenv("PBH_PROF") && cudaMalloc(&h->d_prof, 16 * sizeof(unsigned long long)) == cudaSuccess) {
     cudaMemset(h->d_prof, 0, 16 * sizeof(unsigned long long));
     const unsigned int on = 1;

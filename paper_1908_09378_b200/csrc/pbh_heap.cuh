@@ -101,7 +101,6 @@ struct HeapCta {
     return out;
   }
   DEV bool stale_share_above(u32 num, u32 den) const {
-    if (g_ab_off) return false;
     const u64 stored = content_from(1);
     const u64 lv = s.live > 0 ? (u64)s.live : 0ull;
     const u64 stale = stored > lv ? stored - lv : 0ull;

@@ -1,7 +1,6 @@
-for r in 1 2 3; do
-  for v in on off; do
-    if [ $v = off ]; then export PBH_AB_OFF=1; else unset PBH_AB_OFF; fi
-    timeout 300 python tools/probe_c4.py --ds 1024,65536 --c1 20000 2>&1 | grep cfg | python -c "
+for r in 1 2; do
+  for v in 0 1 2 4; do
+    PBH_AB_OFF=$v timeout 300 python tools/probe_c4.py --ds 256,1024,65536 --c1 20000 2>&1 | grep cfg | python -c "
 import sys, json
 out=[]
 for l in sys.stdin:
