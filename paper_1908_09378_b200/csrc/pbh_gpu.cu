@@ -675,6 +675,11 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
   const u32 bc = (u32)pow2_at_least(std::max<u64>(std::min<u64>(d, 4096), 2));
   auto fail = [&](pbh_status s) {
     h->H.free_all();
+    cudaFree(h->d_job);
+    cudaFree(h->d_save);
+    if (h->h_ks) cudaFreeHost(h->h_ks);
+    if (h->h_mop) cudaFreeHost(h->h_mop);
+    if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
     return s;
   };
