@@ -1,6 +1,6 @@
 for r in 1 2; do
-  for v in 0 1 2 4; do
-    PBH_AB_OFF=$v timeout 300 python tools/probe_c4.py --ds 256,1024,65536 --c1 20000 2>&1 | grep cfg | python -c "
+  for v in 0 1 2 3 5; do
+    PBH_AB_OFF=$v timeout 300 python tools/probe_c4.py --ds 1024,65536 --c1 200000 2>&1 | grep cfg | python -c "
 import sys, json
 out=[]
 for l in sys.stdin:
