@@ -503,6 +503,14 @@ def leg_c4(P, gen, dev, peak, ds, cpu):
 
 
 def leg_api_latency(P, dev, n_calls=2000):
+    """Both single-op modes: persistent (default: a resident kernel serves
+    the calls through mapped host memory) and one launch per call."""
+    out = _api_latency(P, dev, n_calls, 200)
+    out["one_launch_per_call"] = _api_latency(P, dev, n_calls, 0)
+    return out
+
+
+def _api_latency(P, dev, n_calls, idle_us):
     """Per-call cost of the single-client Engine API through the C-ABI
     (engine.cpp:90-109: update, bulk_update, extract_min, delete_value): host
     wall time per blocking call, heap of 2^20 keys at d = 32 (the latency
@@ -515,6 +523,7 @@ def leg_api_latency(P, dev, n_calls=2000):
         warm.extract_min()
     warm.close()
     eng = P.Engine(P.EngineConfig(d=32, debug_assertions=False, key_universe=1 << 20, device=dev))
+    eng.set_persistent(idle_us)
     rng = np.random.default_rng(3)
     keys = rng.permutation(1 << 20).astype(np.uint32)
     out = {}
@@ -536,6 +545,15 @@ def leg_api_latency(P, dev, n_calls=2000):
     for i in range(n_calls):
         eng.delete_value(int(keys[i]))
     out["delete_us"] = (_t.perf_counter() - t0) * 1e6 / n_calls
+    if idle_us:
+        pp = eng.persist_profile()
+        out["mode"] = "persistent (idle %d us)" % idle_us
+        out["kernel_us_per_call"] = {"wait": pp["wait_ns"] / 1e3 / max(pp["requests"], 1),
+                                     "copy_in": pp["copy_ns"] / 1e3 / max(pp["requests"], 1),
+                                     "run": pp["run_ns"] / 1e3 / max(pp["requests"], 1)}
+        out["resident_launches"] = pp["launches"]
+    else:
+        out["mode"] = "one launch per call"
     eng.close()
     out["calls_each"] = n_calls
     return out

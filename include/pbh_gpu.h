@@ -81,6 +81,21 @@ pbh_status pbh_heap_extract_min(pbh_heap* h, uint32_t* value, uint64_t* priority
 pbh_status pbh_heap_find_min(pbh_heap* h, uint32_t* value, uint64_t* priority);
 /* Engine::delete_value(Value) (engine.cpp:106-109): absent -> no-op. */
 pbh_status pbh_heap_delete(pbh_heap* h, uint32_t value);
+/* Latency mode of the single ops above (no reference counterpart; the
+ * reference runs them on the calling thread, engine.cpp:90-109). With
+ * idle_us > 0 (default 200) the first single op leaves one k_trace_bank
+ * resident on the heap's stream: later single ops are posted to it through
+ * mapped host memory (no launch, no level-0 reload) until it has been idle
+ * for idle_us, when it saves its state and exits. Every other call on the
+ * heap stops it first. idle_us = 0: one launch per single op. idle_us above
+ * 10^7 -> PBH_PRECONDITION. */
+pbh_status pbh_heap_set_persistent(pbh_heap* h, uint64_t idle_us);
+/* Latency profile of persistent mode: out[0] requests served by resident
+ * kernels, out[1] resident kernels launched, out[2..4] nanoseconds the
+ * resident kernels spent waiting for requests, copying them in and running
+ * them (cumulative; out[2..4] are current once the heap has been stopped by
+ * any non-single-op call or the kernel's idle exit). */
+pbh_status pbh_heap_persist_profile(pbh_heap* h, uint64_t out[5]);
 /* Engine::live_size() (engine.hpp:61). */
 pbh_status pbh_heap_live_size(pbh_heap* h, int64_t* n);
 /* Engine::drain() (engine.cpp:138-150): flush all signal buffers. */

@@ -162,6 +162,8 @@ class Engine {
     return n;
   }
   void drain() { detail::check(pbh_heap_drain(h_)); }
+  // latency mode of the single ops (pbh_heap_set_persistent; 0 = one launch per op)
+  void set_persistent(std::uint64_t idle_us) { detail::check(pbh_heap_set_persistent(h_, idle_us)); }
   Metrics snapshot_metrics() const {
     Metrics m;
     std::vector<std::uint64_t> r(PBH_GPU_MAX_LEVELS), t(PBH_GPU_MAX_LEVELS);

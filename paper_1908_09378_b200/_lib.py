@@ -38,6 +38,8 @@ SIGNATURES = {
     "pbh_heap_extract_min": (C.c_int, [C.c_void_p, U32P, U64P]),
     "pbh_heap_find_min": (C.c_int, [C.c_void_p, U32P, U64P]),
     "pbh_heap_delete": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "pbh_heap_set_persistent": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "pbh_heap_persist_profile": (C.c_int, [C.c_void_p, U64P]),
     "pbh_heap_live_size": (C.c_int, [C.c_void_p, I64P]),
     "pbh_heap_drain": (C.c_int, [C.c_void_p]),
     "pbh_heap_metrics": (C.c_int, [C.c_void_p, U64P, U64P, U64P, U32P]),

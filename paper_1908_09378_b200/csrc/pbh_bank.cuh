@@ -1315,7 +1315,8 @@ template <int NW, int KI, int VT>
 __global__ void __launch_bounds__(32 * NW, 1)
     k_trace_bank(pbh_heap_dev* g, pbh_trace_dev tr, u64 op_begin, u64 op_end, u32* out_v,
                  u64* out_p, pbh_kstatus* ks, BankL0<32 * NW, KI>* save, u32 allow_internal,
-                 GridJob* gj, u32 grid_min, unsigned long long* prof, BatchJob* bj) {
+                 GridJob* gj, u32 grid_min, unsigned long long* prof, BatchJob* bj,
+                 pbh_op_channel* pm) {
   using BH = BankHeap<NW, KI, VT>;
   using HC = typename BH::HC;
   using Bk = Blk<BH::B>;
@@ -1428,7 +1429,116 @@ __global__ void __launch_bounds__(32 * NW, 1)
   u64 ea = op < op_end ? tr.offsets[op + 1] : 0;
   u8 kb = op + 1 < op_end ? tr.kinds[op + 1] : 0;
   u64 eb = op + 1 < op_end ? tr.offsets[op + 2] : 0;
-  for (; op < op_end; ++op) {
+  // persistent mode (pm != null): requests are served one after another from
+  // the mapped channel. Every channel word is a flagged word (request number
+  // in the high 32 bits, payload in the low 32), so a word is valid exactly
+  // when it carries the expected number: no fences on either side, one PCIe
+  // round trip to read a single-element request, none to publish a result.
+  u32 seq = pm ? (u32)(pm->rs[0] >> 32) : 0;  // last request served
+  __shared__ u32 s_ctl, s_hdr, s_v;  // leader's wait verdict and the request header
+  __shared__ u64 s_p;
+  bool in_req = false;  // a request is being served (its result is still owed)
+  // thread 0: wait / copy / run (ns), cumulative over the heap's resident kernels
+  u64 tw = 0, tc = 0, tx = 0, t_seen = 0, t_cop = 0;
+  if (pm && tid == 0) {
+    tw = pm->tprof[0];
+    tc = pm->tprof[1];
+    tx = pm->tprof[2];
+  }
+  for (;; ++op) {
+    if (op >= op_end) {
+      if (!pm) break;
+      if (in_req && tid == 0) {
+        // the finished request's result record
+        const u64 sq = (u64)seq << 32;
+        const u32 ov = n_out ? out_v[0] : 0;
+        const u64 opr = n_out ? out_p[0] : 0;
+        u64 t2;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+        tc += t_cop - t_seen;
+        tx += t2 - t_cop;
+        asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(&pm->rs[0]),
+                     "l"(sq | (u32)n_out), "l"(sq | ov) : "memory");
+        asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(&pm->rs[2]),
+                     "l"(sq | (u32)opr), "l"(sq | (u32)(opr >> 32)) : "memory");
+        pm->tprof[0] = tw;
+        pm->tprof[1] = tc;
+        pm->tprof[2] = tx;
+      }
+      in_req = false;
+      if (tid == 0) {
+        u64 t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        const u64 idle = pm->idle_ns;
+        const u32 want = seq + 1;
+        u32 cmd = 0;
+        for (;;) {
+          u64 a0, a1, a2, a3, stp;
+          asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a0), "=l"(a1) : "l"(&pm->rq[0]));
+          asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a2), "=l"(a3) : "l"(&pm->rq[2]));
+          stp = pm->stop;
+          if (stp) break;
+          if ((u32)(a0 >> 32) == want && (u32)(a1 >> 32) == want && (u32)(a2 >> 32) == want &&
+              (u32)(a3 >> 32) == want) {
+            cmd = 1;
+            s_hdr = (u32)a0;
+            s_v = (u32)a1;
+            s_p = (u64)(u32)a2 | (a3 << 32);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_seen));
+            tw += t_seen - t0;
+            break;
+          }
+          u64 t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+          if (t1 - t0 > idle) break;
+        }
+        s_ctl = cmd;
+      }
+      Bk::sync();
+      if (s_ctl == 0) break;
+      // the op into device staging (the engine reads staging written by
+      // this CTA); a multi-element payload is read until every word carries
+      // the request number
+      ++seq;
+      const u32 hdr = s_hdr;
+      const u32 n = hdr >> 8;
+      u32* sv = const_cast<u32*>(tr.vals);
+      u64* sp = const_cast<u64*>(tr.prios);
+      if (n == 1) {
+        if (tid == 0) {
+          sv[0] = s_v;
+          sp[0] = s_p;
+        }
+      } else if (n > 1) {
+        for (;;) {
+          bool ok = true;
+          for (u32 i = tid; i < n; i += B) {
+            const u64 w0 = pm->rv[i], w1 = pm->rplo[i], w2 = pm->rphi[i];
+            ok &= (u32)(w0 >> 32) == seq && (u32)(w1 >> 32) == seq && (u32)(w2 >> 32) == seq;
+            sv[i] = (u32)w0;
+            sp[i] = (u64)(u32)w1 | (w2 << 32);
+          }
+          if (__syncthreads_and(ok)) break;
+        }
+      }
+      if (tid == 0) {
+        const_cast<u8*>(tr.kinds)[0] = (u8)hdr;
+        const_cast<u64*>(tr.offsets)[0] = 0;
+        const_cast<u64*>(tr.offsets)[1] = n;
+      }
+      __threadfence_block();
+      Bk::sync();
+      if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_cop));
+      in_req = true;
+      n_out = 0;
+      op = 0;
+      op_end = 1;
+      hs_ = 0;
+      ka = (u8)hdr;
+      ea = n;
+      kb = 0;
+      eb = 0;
+    }
     const u8 kind = ka;
     const u64 ob = hs_, oe = ea;
     if (tid == 0 && op + 1 < op_end && eb > ea) {
@@ -1852,13 +1962,18 @@ __global__ void __launch_bounds__(32 * NW, 1)
   trace_image_copy<B, KI>(*save, L, false);
   H.to_cold();
   hc.store();
-  if (tid == 0) {
+  if (tid == 0 && (!pm || in_req)) {
     ks->status = sm.status;
     ks->detail = sm.detail;
     ks->aux = sm.aux;
     ks->ops_done = op - op_begin;
     ks->n_out = n_out;
     ks->failed_op = op;
+    if (pm) {
+      // a failed request: its result record says so; the host resolves it
+      // (index growth, error) from the status block after this launch ends
+      pm->rs[0] = ((u64)seq << 32) | 0xFFFFFFFFu;
+    }
   }
 }
 

@@ -46,8 +46,11 @@ pbh_status set_err(pbh_status s, const std::string& msg) {
 constexpr int VT = 4;
 constexpr u32 kOorCap = 4096;  // remembered out-of-index deletes per heap
 constexpr size_t kTmaSlack = 64;  // bytes past each merge buffer (TMA window over-read)
-constexpr u32 kInlineOpMax = 256;  // single ops up to this many elements read from mapped host memory
+constexpr u32 kInlineOpMax = PBH_INLINE_OP_MAX;  // single ops up to this many elements read from mapped host memory
 constexpr u64 kSoloMax = 1ull << 16;  // single ops on one CTA while fewer entries were inserted
+constexpr u64 kPersistIdleNs = 200000;
+static_assert(offsetof(pbh_op_channel, rq) % 16 == 0 && offsetof(pbh_op_channel, rs) % 16 == 0,
+              "flagged channel words are read / written as 16-byte pairs");  // a persistent single-op kernel exits after 200 us idle
 
 u64 pow2_at_least(u64 x) {
   u64 p = 1;
@@ -78,7 +81,7 @@ using TraceSmem = TraceBankSmem<kTraceNW, kTraceKI, VT>;
 cudaError_t launch_trace_bank(cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr, u64 b, u64 e,
                               u32* ov, u64* op, pbh_kstatus* ks, TraceImage* save, u32 internal,
                               GridJob* gj, u32 grid_min, unsigned long long* prof,
-                              BatchJob* bj, bool solo) {
+                              BatchJob* bj, bool solo, pbh_op_channel* pm = nullptr) {
   auto fn = k_trace_bank<kTraceNW, kTraceKI, VT>;
   const int smem = (int)sizeof(TraceSmem);
   cudaError_t err = cudaSuccess;
@@ -102,11 +105,11 @@ cudaError_t launch_trace_bank(cudaStream_t st, pbh_heap_dev* g, pbh_trace_dev tr
     // the job word and the job-barrier counter restart with every launch
     err = cudaMemsetAsync(gj, 0, sizeof(GridJob), st);
     if (err != cudaSuccess) return err;
-    void* args[] = {&g, &tr, &b, &e, &ov, &op, &ks, &save, &internal, &gj, &grid_min, &prof, &bj};
+    void* args[] = {&g, &tr, &b, &e, &ov, &op, &ks, &save, &internal, &gj, &grid_min, &prof, &bj, &pm};
     err = cudaLaunchCooperativeKernel((const void*)fn, dim3(G), dim3(32 * kTraceNW), args, smem, st);
   } else {
     fn<<<1, 32 * kTraceNW, smem, st>>>(g, tr, b, e, ov, op, ks, save, internal, gj, grid_min,
-                                       prof, nullptr);
+                                       prof, nullptr, pm);
     err = cudaGetLastError();
   }
   g_launches++;
@@ -426,16 +429,16 @@ struct pbh_heap {
   pbh_kstatus* h_ks = nullptr;  // status block in mapped pinned host memory (written by the kernel)
   // single ops (the Engine's per-call API): their inputs and outputs live in
   // mapped pinned host memory the kernel reads / writes directly (no copies)
-  struct MappedOp {
-    u8 kinds[16];
-    u64 off[2];
-    u32 vals[kInlineOpMax];
-    u64 prios[kInlineOpMax];
-    u32 out_v[1];
-    u64 out_p[1];
-  };
-  MappedOp* h_mop = nullptr;
-  MappedOp* d_mop = nullptr;
+  pbh_op_channel* h_mop = nullptr;
+  pbh_op_channel* d_mop = nullptr;
+  // persistent single-op kernel (pbh_heap_set_persistent): resident while
+  // `alive`, `seq` requests posted so far, launched as one CTA if `alive_solo`
+  u64 persist_idle_ns = kPersistIdleNs;
+  bool alive = false;
+  bool alive_solo = false;
+  u64 seq = 0;
+  u64 persist_reqs = 0;     // requests served by resident kernels
+  u64 persist_launches = 0; // resident kernels launched
   // entries inserted so far (an upper bound of what the heap stores): while
   // small, single ops launch one CTA (their merges are short) instead of
   // the cooperative grid
@@ -486,12 +489,26 @@ pbh_status ensure_staging(pbh_heap* h, u64 n_ops, u64 n_el, u64 n_out) {
   return PBH_OK;
 }
 
+// Stop a resident persistent single-op kernel (its level-0 image and heap
+// state are saved when it exits): every path that launches another kernel
+// on the heap or reads its device state calls this first.
+pbh_status quiesce(pbh_heap* h) {
+  if (!h->alive) return PBH_OK;
+  h->alive = false;
+  h->h_mop->stop = 1;
+  const cudaError_t e = cudaStreamSynchronize(h->stream);
+  h->h_mop->stop = 0;
+  if (e != cudaSuccess) return set_err(PBH_CUDA, cudaGetErrorString(e));
+  return PBH_OK;
+}
+
 // Run ops [0, n_ops) of a device trace with the NEED_GROW / KEY_RANGE resume
 // loop. host_vals: host copy of the values (for universe growth) or null.
 pbh_status exec_trace(pbh_heap* h, u64 n_ops, pbh_trace_dev tr, u32* d_ov, u64* d_op,
                       u64* n_out, u64* failed_op, u32 internal, double* wall_ms,
                       const u8* host_kinds, const u64* host_off, const u32* host_vals,
                       bool solo = false) {
+  if (pbh_status q = quiesce(h)) return q;
   // the status block is mapped host memory: the stream is idle between
   // calls, so the host resets it directly and reads the kernel's writes
   // after the synchronize
@@ -621,7 +638,84 @@ pbh_status single_op(pbh_heap* h, u8 kind, const u32* vals, const u64* prios, u6
                      u64* op) {
   u64 off[2] = {0, n};
   u64 got = 0;
-  pbh_status st;
+  pbh_status st = PBH_OK;
+  if (n <= kInlineOpMax && !h->d_prof && h->persist_idle_ns) {
+    // persistent: post the op to the resident kernel (launched if it is not
+    // running) and spin on its acknowledgement
+    auto* m = h->h_mop;
+    const bool solo = h->inserted + n < kSoloMax;
+    if (h->alive && h->alive_solo && !solo)
+      if ((st = quiesce(h))) return st;  // grown past one CTA: relaunch on the grid
+    // flagged words: payload first, header last (each word validates itself)
+    const u32 s = (u32)++h->seq;
+    const u64 sq = (u64)s << 32;
+    if (n > 1)
+      for (u64 i = 0; i < n; ++i) {
+        m->rv[i] = sq | vals[i];
+        m->rplo[i] = sq | (u32)prios[i];
+        m->rphi[i] = sq | (u32)(prios[i] >> 32);
+      }
+    const u64 p1 = n == 1 ? prios[0] : 0;
+    m->rq[1] = sq | (n == 1 ? vals[0] : 0u);
+    m->rq[2] = sq | (u32)p1;
+    m->rq[3] = sq | (u32)(p1 >> 32);
+    m->rq[0] = sq | kind | (u32)(n << 8);
+    auto launch = [&]() -> pbh_status {
+      if ((st = ensure_staging(h, 1, kInlineOpMax, 1))) return st;
+      std::memset(h->h_ks, 0, sizeof(pbh_kstatus));
+      m->idle_ns = h->persist_idle_ns;
+      pbh_trace_dev tr{h->d_kinds, h->d_off, h->d_vals, h->d_prios};
+      CK(launch_trace_bank(h->stream, h->H.dev, tr, 0, 0, h->d_ov, h->d_op, h->d_ks, h->d_save, 1,
+                           h->d_job, h->grid_min, nullptr, h->d_batch, solo, h->d_mop));
+      h->alive = true;
+      h->alive_solo = solo || !h->d_job;
+      h->persist_launches++;
+      return PBH_OK;
+    };
+    if (!h->alive && (st = launch())) return st;
+    // the kernel exits on its own after idle_ns: a request posted as it left
+    // is found unserved on an idle stream and served by a relaunch
+    int relaunches = 0;
+    u64 r0;
+    for (u32 spin = 1; (u32)((r0 = m->rs[0]) >> 32) != s; ++spin) {
+      if (spin % 256) continue;
+      const cudaError_t q = cudaStreamQuery(h->stream);
+      if (q == cudaErrorNotReady) continue;
+      if (q != cudaSuccess) {
+        h->alive = false;
+        return set_err(PBH_CUDA, cudaGetErrorString(q));
+      }
+      if ((u32)(m->rs[0] >> 32) == s) continue;
+      h->alive = false;
+      if (++relaunches > 2)
+        return set_err(PBH_INVARIANT, "persistent kernel exited without serving the request");
+      if ((st = launch())) return st;
+    }
+    h->persist_reqs++;
+    if ((u32)r0 != 0xFFFFFFFFu) {
+      if (kind == 'U' || kind == 'B') h->inserted += n;
+      got = (u32)r0;
+      if ((kind == 'E' || kind == 'F') && got != 1)
+        return set_err(PBH_INVARIANT, "extract produced no element");
+      if (got) {
+        u64 r1, r2, r3;
+        do {
+          r1 = m->rs[1];
+          r2 = m->rs[2];
+          r3 = m->rs[3];
+        } while ((u32)(r1 >> 32) != s || (u32)(r2 >> 32) != s || (u32)(r3 >> 32) != s);
+        if (ov) {
+          *ov = (u32)r1;
+          *op = (u64)(u32)r2 | (r3 << 32);
+        }
+      }
+      return PBH_OK;
+    }
+    // a failed op (nothing of it applied): the kernel has exited; the
+    // one-shot path below re-runs it with index growth and error reporting
+    CK(cudaStreamSynchronize(h->stream));
+    h->alive = false;
+  }
   if (n <= kInlineOpMax && !h->d_prof) {
     // zero-copy: the op and its elements in mapped host memory, the
     // extraction written straight back there
@@ -696,9 +790,13 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
   if (st) return fail(st);
   if (cudaHostAlloc(&h->h_ks, sizeof(pbh_kstatus), cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer(&h->d_ks, h->h_ks, 0) != cudaSuccess ||
-      cudaHostAlloc(&h->h_mop, sizeof(pbh_heap::MappedOp), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc(&h->h_mop, sizeof(pbh_op_channel), cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer(&h->d_mop, h->h_mop, 0) != cudaSuccess)
     return fail(set_err(PBH_OOM, "status block allocation failed"));
+  // pinned allocations are not zeroed: the channel's req / ack counters
+  // must start equal (no request posted)
+  std::memset(h->h_ks, 0, sizeof(pbh_kstatus));
+  std::memset(h->h_mop, 0, sizeof(pbh_op_channel));
   // grid helpers for the deep merges (PBH_GRID=1 disables them)
   const char* ge = getenv("PBH_GRID");
   if (!(ge && atoi(ge) <= 1) && cudaMalloc(&h->d_job, sizeof(GridJob)) != cudaSuccess)
@@ -756,6 +854,7 @@ pbh_status pbh_heap_create(uint64_t d, uint64_t key_universe, int device, int de
 pbh_status pbh_heap_destroy(pbh_heap* h) {
   if (!h) return PBH_OK;
   cudaSetDevice(h->device);
+  quiesce(h);
   cudaStreamSynchronize(h->stream);
   h->H.free_all();
   cudaFreeHost(h->h_ks);
@@ -834,9 +933,30 @@ pbh_status pbh_heap_delete(pbh_heap* h, uint32_t value) {
   return single_op(h, 'D', &value, &dummy, 1, nullptr, nullptr);
 }
 
+pbh_status pbh_heap_set_persistent(pbh_heap* h, uint64_t idle_us) {
+  if (!h) return set_err(PBH_PRECONDITION, "null heap");
+  if (idle_us > 10000000) return set_err(PBH_PRECONDITION, "persistent idle time above 10 s");
+  cudaSetDevice(h->device);
+  if (pbh_status q = quiesce(h)) return q;
+  h->persist_idle_ns = idle_us * 1000;
+  return PBH_OK;
+}
+
+pbh_status pbh_heap_persist_profile(pbh_heap* h, uint64_t out[5]) {
+  if (!h || !out) return set_err(PBH_PRECONDITION, "null argument");
+  out[0] = h->persist_reqs;
+  out[1] = h->persist_launches;
+  // cumulative over the resident kernel's life (reset at each launch)
+  out[2] = h->h_mop->tprof[0];
+  out[3] = h->h_mop->tprof[1];
+  out[4] = h->h_mop->tprof[2];
+  return PBH_OK;
+}
+
 pbh_status pbh_heap_live_size(pbh_heap* h, int64_t* n) {
   if (!h || !n) return set_err(PBH_PRECONDITION, "null argument");
   cudaSetDevice(h->device);
+  if (pbh_status q = quiesce(h)) return q;
   CK(cudaMemcpyAsync(n, &h->H.dev->live, 8, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   return PBH_OK;
@@ -852,6 +972,7 @@ pbh_status pbh_heap_metrics(pbh_heap* h, uint64_t* ops, uint64_t* resolves, uint
                             uint32_t* n_levels) {
   if (!h) return set_err(PBH_PRECONDITION, "null heap");
   cudaSetDevice(h->device);
+  if (pbh_status q = quiesce(h)) return q;
   pbh_heap_dev hd;
   CK(cudaMemcpyAsync(&hd, h->H.dev, sizeof(hd), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
@@ -871,6 +992,7 @@ pbh_status pbh_heap_metrics(pbh_heap* h, uint64_t* ops, uint64_t* resolves, uint
 pbh_status pbh_heap_stats(pbh_heap* h, uint64_t* stored_deep, uint64_t* stale_dropped) {
   if (!h) return set_err(PBH_PRECONDITION, "null heap");
   cudaSetDevice(h->device);
+  if (pbh_status q = quiesce(h)) return q;
   pbh_heap_dev hd;
   CK(cudaMemcpyAsync(&hd, h->H.dev, sizeof(hd), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
@@ -884,6 +1006,7 @@ pbh_status pbh_heap_stats(pbh_heap* h, uint64_t* stored_deep, uint64_t* stale_dr
 pbh_status pbh_heap_check_invariants(pbh_heap* h, uint64_t* n_violations) {
   if (!h || !n_violations) return set_err(PBH_PRECONDITION, "null argument");
   cudaSetDevice(h->device);
+  if (pbh_status q = quiesce(h)) return q;
   pbh_heap_dev hd;
   CK(cudaMemcpyAsync(&hd, h->H.dev, sizeof(hd), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));

@@ -90,6 +90,39 @@ typedef struct {
   const uint64_t* prios;
 } pbh_trace_dev;
 
+// Single-op channel of the Engine's per-call API (engine.cpp:90-109), in
+// mapped pinned host memory. One-shot launches read the op from the plain
+// fields and write the extraction back to them. In persistent mode one
+// resident k_trace_bank serves op after op through flagged words (request
+// number << 32 | 32-bit payload; a word is current iff it carries the
+// expected number, so neither side needs a fence):
+//   rq[0] kind | n << 8, rq[1] value, rq[2..3] priority (lo, hi) of a
+//   single-element op; rv / rplo / rphi the elements of a larger one;
+//   rs[0] n_out (0xFFFFFFFF: the op failed, see the status block),
+//   rs[1] extracted value, rs[2..3] its priority.
+// The kernel exits (saving its level-0 image) on `stop`, on a failed op, or
+// after `idle_ns` without a request.
+#define PBH_INLINE_OP_MAX 256
+typedef struct {
+  uint8_t kinds[16];
+  uint64_t off[2];
+  uint32_t vals[PBH_INLINE_OP_MAX];
+  uint64_t prios[PBH_INLINE_OP_MAX];
+  uint32_t out_v[2];
+  uint64_t out_p[1];
+  uint64_t idle_ns;
+  uint64_t tprof[3];  // kernel: ns spent waiting for / copying in / running requests
+  volatile uint64_t rq[4];
+  uint64_t pad1[4];
+  volatile uint64_t rs[4];
+  uint64_t pad2[4];
+  volatile uint64_t stop;
+  uint64_t pad3[7];
+  volatile uint64_t rv[PBH_INLINE_OP_MAX];
+  volatile uint64_t rplo[PBH_INLINE_OP_MAX];
+  volatile uint64_t rphi[PBH_INLINE_OP_MAX];
+} pbh_op_channel;
+
 // Kernel status block (device memory, read back by the host).
 typedef struct {
   uint32_t status;      // pbh_status

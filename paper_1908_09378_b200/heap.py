@@ -132,6 +132,19 @@ class Engine:
     def delete_value(self, value: int):
         raise_for(_lib.lib().pbh_heap_delete(self._h, int(value)))
 
+    def set_persistent(self, idle_us: int = 200):
+        """Latency mode of the single ops (pbh_heap_set_persistent): a
+        resident kernel serves them through mapped host memory until idle
+        for ``idle_us``; 0 launches one kernel per op."""
+        raise_for(_lib.lib().pbh_heap_set_persistent(self._h, int(idle_us)))
+
+    def persist_profile(self) -> dict:
+        """pbh_heap_persist_profile: requests served by resident kernels,
+        launches, and the resident kernel's wait / copy-in / run time (ns)."""
+        o = np.zeros(5, np.uint64)
+        raise_for(_lib.lib().pbh_heap_persist_profile(self._h, _ptr(o, U64P)))
+        return dict(zip(["requests", "launches", "wait_ns", "copy_ns", "run_ns"], map(int, o)))
+
     def live_size(self) -> int:
         n = C.c_int64()
         raise_for(_lib.lib().pbh_heap_live_size(self._h, C.byref(n)))
