@@ -1,4 +1,6 @@
-# persistent single-op API: latency probe, then the whole GPU suite
+# SSSP engine width A/B on the grid (degree 4) and the band (degree 256)
 export PYTHONPATH=.
-timeout 600 python tools/probe_api.py --calls 2000 --pre 0,100000 2>&1 | tail -6
-timeout 1500 python -m pytest -x -q -m gpu tests -p no:cacheprovider 2>&1 | tail -5
+for nw in 4 2 1 8 4; do
+  PBH_SSSP_NW=$nw timeout 300 python tools/probe_sssp.py exact grid 2048 2 2>&1 | tail -1 | sed "s/^/nw=$nw /" | cut -c1-200
+  PBH_SSSP_NW=$nw timeout 300 python tools/probe_sssp.py exact band 18 1 2>&1 | tail -1 | sed "s/^/nw=$nw /" | cut -c1-200
+done
