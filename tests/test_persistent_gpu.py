@@ -113,3 +113,41 @@ def test_set_persistent_rejects_huge_idle(pbh):
     with pytest.raises(pbh.PreconditionError):
         eng.set_persistent(10 ** 8)
     eng.close()
+
+
+@pytest.mark.timeout(300)
+def test_two_resident_engines_and_sssp_interleaved(pbh, O):
+    # two heaps alternate call by call (each call waits for the other heap's
+    # resident kernel to go idle), with an SSSP solve on the same device in
+    # between: every result still matches the oracle
+    from paper_1908_09378_b200 import gen
+    tr_a = O.gen_legal_trace(400, 8, 11)
+    tr_b = O.gen_legal_trace(400, 8, 12)
+    want_a, _ = O.run_oracle(tr_a)
+    want_b, _ = O.run_oracle(tr_b)
+    engs = [pbh.Engine(pbh.EngineConfig(d=8, debug_assertions=True)) for _ in range(2)]
+    outs = [[], []]
+    g = gen.grid(32, 32, 3)
+    want_dist = O.dijkstra(O.Graph(g.vertex_count, g.offsets, g.targets, g.weights), 0)["dist"]
+    for i in range(max(tr_a.n_ops, tr_b.n_ops)):
+        for which, tr in enumerate((tr_a, tr_b)):
+            if i >= tr.n_ops:
+                continue
+            k, b = int(tr.kinds[i]), int(tr.offsets[i])
+            e = int(tr.offsets[i + 1])
+            eng = engs[which]
+            if k == ord("U"):
+                eng.update((int(tr.vals[b]), int(tr.prios[b])))
+            elif k == ord("B"):
+                eng.bulk_update(values=tr.vals[b:e], priorities=tr.prios[b:e])
+            elif k == ord("E"):
+                outs[which].append(tuple(eng.extract_min())[0])
+            elif k == ord("D"):
+                eng.delete_value(int(tr.vals[b]))
+        if i == 200:
+            r = pbh.par_dijkstra(g, 0)
+            assert np.array_equal(np.asarray(r.dist), want_dist)
+    assert np.array_equal(np.array(outs[0], np.uint32), want_a)
+    assert np.array_equal(np.array(outs[1], np.uint32), want_b)
+    for eng in engs:
+        eng.close()
