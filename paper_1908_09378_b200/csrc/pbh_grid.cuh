@@ -21,8 +21,18 @@
 
 namespace pbh_dev {
 
-constexpr u32 kGridTile = 2048;   // outputs per streamed tile
-constexpr u32 kGridMin = 2048;    // smallest merge worth a grid job (measured sweep 2K..16K: 2K best)
+#ifndef PBH_GRID_TILE
+// 5 outputs per thread: an odd per-thread stride keeps the merge-path reads
+// and the staging writes off the bank conflicts of a stride of 8 four- /
+// eight-byte entries (2048 = 8 per thread and 1792 = 7 measured slower on
+// C1, C4 d = 32 and d = 1024; 1792 is 3 % faster at d = 65536)
+#define PBH_GRID_TILE 1280
+#endif
+constexpr u32 kGridTile = PBH_GRID_TILE;  // outputs per streamed tile
+#ifndef PBH_GRID_MIN_MERGE
+#define PBH_GRID_MIN_MERGE 2048
+#endif
+constexpr u32 kGridMin = PBH_GRID_MIN_MERGE;  // smallest merge worth a grid job (measured sweep 2K..16K: 2K best)
 constexpr u32 kStreamMin = 64;    // smallest merge streamed through the windows by one CTA
 
 // Sort n entries (K, P) in shared memory by (p, k) with the whole CTA (K, P,
@@ -249,7 +259,10 @@ struct BatchJob {
 };
 constexpr u32 kBucketMax = 1184;  // 8 buckets per CTA of a 148-CTA grid
 constexpr u32 kRankSortMax = 192;  // buckets up to this size: rank sort (measured vs cta_sort)
-constexpr u32 kBulkStoreMin = 1024;  // merge tiles at least this large leave by bulk stores
+#ifndef PBH_BULK_STORE_MIN
+#define PBH_BULK_STORE_MIN 1024
+#endif
+constexpr u32 kBulkStoreMin = PBH_BULK_STORE_MIN;  // merge tiles at least this large leave by bulk stores
 
 template <int NT>
 struct GridSmem {

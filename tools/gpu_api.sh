@@ -1,6 +1,15 @@
-# SSSP engine width A/B on the grid (degree 4) and the band (degree 256)
+# A/B of the streamed-merge tile: 7 per thread, 5 per thread, 5 per thread with two staging tiles
 export PYTHONPATH=.
-for nw in 4 2 1 8 4; do
-  PBH_SSSP_NW=$nw timeout 300 python tools/probe_sssp.py exact grid 2048 2 2>&1 | tail -1 | sed "s/^/nw=$nw /" | cut -c1-200
-  PBH_SSSP_NW=$nw timeout 300 python tools/probe_sssp.py exact band 18 1 2>&1 | tail -1 | sed "s/^/nw=$nw /" | cut -c1-200
+for r in 1 2; do
+  for v in vt7 vt5 vt5db; do
+    cp variants/lib_$v.so paper_1908_09378_b200/libpbh_gpu.so
+    timeout 300 python tools/probe_c4.py --ds 32,1024,65536 --c1 100000 2>&1 | grep cfg | python -c "
+import sys, json
+out=[]
+for l in sys.stdin:
+    d=json.loads(l); out.append('%s=%.3f' % (d['cfg']+str(d.get('d','')), d.get('us_per_batch', d.get('us_per_op', 0))))
+print('$v', ' '.join(out))"
+  done
 done
+cp variants/lib_vt5db.so paper_1908_09378_b200/libpbh_gpu.so
+timeout 900 python -m pytest -x -q tests/test_heap_big_gpu.py tests/test_heap_gpu.py tests/test_persistent_gpu.py tests/test_acceptance_gpu.py 2>&1 | tail -3
