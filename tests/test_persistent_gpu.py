@@ -151,3 +151,23 @@ def test_two_resident_engines_and_sssp_interleaved(pbh, O):
     assert np.array_equal(np.array(outs[1], np.uint32), want_b)
     for eng in engs:
         eng.close()
+
+
+def test_resident_kernel_idle_exit_and_modes(pbh):
+    import time
+    eng = pbh.Engine(pbh.EngineConfig(d=8, debug_assertions=True))
+    eng.set_persistent(1000000)  # 1 s: two quick calls share one resident kernel
+    eng.update((1, 10))
+    eng.update((2, 20))
+    assert eng.persist_profile()["launches"] == 1
+    eng.set_persistent(50)  # stops the resident kernel; 50 us idle from now on
+    eng.update((3, 30))
+    time.sleep(0.02)  # the kernel exits after 50 us without a request
+    eng.update((4, 40))
+    pp = eng.persist_profile()
+    assert pp["launches"] == 3 and pp["requests"] == 4
+    eng.set_persistent(0)  # one launch per call: no resident kernel
+    assert tuple(eng.extract_min()) == (1, 10)
+    assert eng.persist_profile()["launches"] == 3
+    assert eng.live_size() == 3
+    eng.close()

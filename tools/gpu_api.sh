@@ -1,7 +1,7 @@
-# A/B of the streamed-merge tile: 7 per thread, 5 per thread, 5 per thread with two staging tiles
+# A/B of the grid-merge threshold (2048 vs 1280 / 4096) and the bulk-store tile minimum (1024 vs 640), interleaved
 export PYTHONPATH=.
 for r in 1 2; do
-  for v in vt7 vt5 vt5db; do
+  for v in base gm1280 gm4096 bs640; do
     cp variants/lib_$v.so paper_1908_09378_b200/libpbh_gpu.so
     timeout 300 python tools/probe_c4.py --ds 32,1024,65536 --c1 100000 2>&1 | grep cfg | python -c "
 import sys, json
@@ -11,5 +11,4 @@ for l in sys.stdin:
 print('$v', ' '.join(out))"
   done
 done
-cp variants/lib_vt5db.so paper_1908_09378_b200/libpbh_gpu.so
-timeout 900 python -m pytest -x -q tests/test_heap_big_gpu.py tests/test_heap_gpu.py tests/test_persistent_gpu.py tests/test_acceptance_gpu.py 2>&1 | tail -3
+cp variants/lib_base.so paper_1908_09378_b200/libpbh_gpu.so
