@@ -699,33 +699,54 @@ DEV void batch_check_classify(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
   const u32 r0 = (u32)((u64)n * b / G), r1 = (u32)((u64)n * (b + 1) / G);
   u32 fresh = 0, bad = 0;
   u64 lo = ~0ull, hi = 0;
-  for (u32 j0 = r0; j0 < r1; j0 += NT) {
-    const u32 j = j0 + threadIdx.x;
-    bool to_leader = false, to_hbm = false;
-    u32 k = 0;
-    u64 p = 0;
-    if (j < r1) {
-      k = vals[j];
-      p = prios[j];
-      if (check && j > 0 && vals[j - 1] >= k) bad |= 1;
-      if (k >= universe) {
+  // two elements per thread per step: both elements' key loads, then both
+  // index gathers are in flight together (one dependent HBM round trip pair
+  // per step instead of per element)
+  constexpr u32 R = 2;
+  for (u32 j0 = r0; j0 < r1; j0 += R * NT) {
+    u32 k[R], kp[R];
+    u64 p[R];
+    ulonglong2 e[R];
+#pragma unroll
+    for (u32 t = 0; t < R; ++t) {
+      const u32 j = j0 + t * NT + threadIdx.x;
+      k[t] = j < r1 ? vals[j] : 0;
+      p[t] = j < r1 ? prios[j] : 0;
+      kp[t] = check && j < r1 && j > 0 ? vals[j - 1] : 0;
+    }
+#pragma unroll
+    for (u32 t = 0; t < R; ++t) {
+      const u32 j = j0 + t * NT + threadIdx.x;
+      e[t] = j < r1 && k[t] < universe ? __ldcg(reinterpret_cast<const ulonglong2*>(idx + k[t]))
+                                       : make_ulonglong2(0, 0);
+    }
+    bool to_leader[R], to_hbm[R];
+    u32 cnt = 0;
+#pragma unroll
+    for (u32 t = 0; t < R; ++t) {
+      const u32 j = j0 + t * NT + threadIdx.x;
+      to_leader[t] = to_hbm[t] = false;
+      if (j >= r1) continue;
+      if (check && j > 0 && kp[t] >= k[t]) bad |= 1;
+      if (k[t] >= universe) {
         bad |= 2;
-      } else {
-        const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(idx + k));
-        const u32 st = (u32)e.y;
-        if (PBH_ST(st) == PBH_ST_DEAD) bad |= 4;
-        if (debug && PBH_ST(st) == PBH_ST_LIVE && p > e.x) bad |= 8;
-        const bool fr = PBH_ST(st) != PBH_ST_LIVE;
-        if (fr || p < e.x) {
-          const bool adm = spl_inf || p < spl_p || (p == spl_p && k <= spl_k);
-          if ((!fr && (st >> 2) < c0) || adm) {
-            to_leader = true;
-          } else {
-            to_hbm = true;
-            fresh += fr;
-            lo = min(lo, p);
-            hi = max(hi, p);
-          }
+        continue;
+      }
+      const u32 st = (u32)e[t].y;
+      if (PBH_ST(st) == PBH_ST_DEAD) bad |= 4;
+      if (debug && PBH_ST(st) == PBH_ST_LIVE && p[t] > e[t].x) bad |= 8;
+      const bool fr = PBH_ST(st) != PBH_ST_LIVE;
+      if (fr || p[t] < e[t].x) {
+        const bool adm = spl_inf || p[t] < spl_p || (p[t] == spl_p && k[t] <= spl_k);
+        if ((!fr && (st >> 2) < c0) || adm) {
+          to_leader[t] = true;
+          cnt += 1;
+        } else {
+          to_hbm[t] = true;
+          cnt += 1u << 16;
+          fresh += fr;
+          lo = min(lo, p[t]);
+          hi = max(hi, p[t]);
         }
       }
     }
@@ -733,17 +754,22 @@ DEV void batch_check_classify(BatchJob* X, u32 b, u32 G, GridSmem<NT>& g) {
     // counter per warp costs more than the CTA scan): leader-list count in
     // the low 16 bits, staging count in the high 16 bits
     u32 tot;
-    const u32 mine = Blk<NT>::scan_excl((to_leader ? 1u : 0u) | (to_hbm ? 1u << 16 : 0u), tot, g.scr);
+    u32 mine = Blk<NT>::scan_excl(cnt, tot, g.scr);
     if (threadIdx.x == 0) {
       g.ok[0] = (tot & 0xffffu) ? atomicAdd(&X->ll_n, tot & 0xffffu) : 0u;
       g.ok[1] = (tot >> 16) ? atomicAdd(&X->stg_n, tot >> 16) : 0u;
     }
     Blk<NT>::sync();
-    if (to_leader) ll[g.ok[0] + (mine & 0xffffu)] = j;
-    if (to_hbm) {
-      const u32 hs = g.ok[1] + (mine >> 16);
-      stg_k[hs] = k;
-      stg_p[hs] = p;
+    u32 ml = g.ok[0] + (mine & 0xffffu), mh = g.ok[1] + (mine >> 16);
+#pragma unroll
+    for (u32 t = 0; t < R; ++t) {
+      const u32 j = j0 + t * NT + threadIdx.x;
+      if (to_leader[t]) ll[ml++] = j;
+      if (to_hbm[t]) {
+        stg_k[mh] = k[t];
+        stg_p[mh] = p[t];
+        ++mh;
+      }
     }
     Blk<NT>::sync();
   }

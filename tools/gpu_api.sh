@@ -1,9 +1,10 @@
-# A/B of the grid-merge threshold (2048 vs 1280 / 4096) and the bulk-store tile minimum (1024 vs 640), interleaved
+# A/B: check + classify job with two elements per thread per step (cc2) vs one (base), interleaved; then parity
 export PYTHONPATH=.
+cp paper_1908_09378_b200/libpbh_gpu.so variants/lib_cc2.so
 for r in 1 2; do
-  for v in base gm1280 gm4096 bs640; do
+  for v in base cc2; do
     cp variants/lib_$v.so paper_1908_09378_b200/libpbh_gpu.so
-    timeout 300 python tools/probe_c4.py --ds 32,1024,65536 --c1 100000 2>&1 | grep cfg | python -c "
+    timeout 300 python tools/probe_c4.py --ds 8192,65536 --c1 0 2>&1 | grep cfg | python -c "
 import sys, json
 out=[]
 for l in sys.stdin:
@@ -11,4 +12,5 @@ for l in sys.stdin:
 print('$v', ' '.join(out))"
   done
 done
-cp variants/lib_base.so paper_1908_09378_b200/libpbh_gpu.so
+cp variants/lib_cc2.so paper_1908_09378_b200/libpbh_gpu.so
+timeout 900 python -m pytest -x -q tests/test_heap_big_gpu.py tests/test_heap_gpu.py tests/test_boundary_gpu.py 2>&1 | tail -3
