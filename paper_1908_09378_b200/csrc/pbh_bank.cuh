@@ -80,6 +80,12 @@ struct __align__(16) LeanOffer {
   u32 c0, c1, pad0, pad1;
 };
 
+#ifndef PBH_MULTI_B0_EIGHTHS
+#define PBH_MULTI_B0_EIGHTHS 6  // threshold engine's B_0: 3/4 of level 0
+#endif
+// 5/8 measured equal on the 2048² grid; 7/8 leaves a refill no free slot
+// (invariant site 0xE5), so the bound is 3/4
+static_assert(PBH_MULTI_B0_EIGHTHS >= 1 && PBH_MULTI_B0_EIGHTHS <= 6, "threshold B_0 above 3/4 of level 0");
 template <int NW, int KI, int VT, bool MW = false>
 struct BankSmem {
   static constexpr int B = 32 * NW;
@@ -89,7 +95,7 @@ struct BankSmem {
   // sort scratch of evict(). A refill pulls up to its capacity: C0/2, or
   // 3/4 of C0 for the threshold engine (its batches drain level 0 fast;
   // fewer, larger refills)
-  static constexpr int B0CAP = MW ? (C0 * 3) / 4 : C0 / 2;
+  static constexpr int B0CAP = MW ? (C0 * PBH_MULTI_B0_EIGHTHS) / 8 : C0 / 2;
   u32 bk[2][B0CAP];
   u64 bp[2][B0CAP];
   u32 sk[kBankQ];  // sort scratch of the push-buffer flush

@@ -129,7 +129,7 @@ struct BankCfg<4> { static constexpr int KI = 8; };
 template <>
 struct BankCfg<8> { static constexpr int KI = 4; };
 constexpr int kBankC0 = 1024;
-constexpr u32 kMultiCap0 = kBankC0 * 3 / 4;  // threshold engine's B_0 (BankSmem<..., true>::B0CAP)
+constexpr u32 kMultiCap0 = kBankC0 * PBH_MULTI_B0_EIGHTHS / 8;  // threshold engine's B_0 (BankSmem<..., true>::B0CAP)
 static_assert(kMultiCap0 == (u32)BankSmem<4, 8, VT, true>::B0CAP, "threshold B_0 capacity");
 static_assert(kBankC0 / 2 == BankSmem<4, 8, VT, false>::B0CAP, "exact B_0 capacity");
 
