@@ -1,9 +1,6 @@
-# pipelined e2e: quick 1-rank bench (C5 + parity) and the 2-rank functional run on one GPU
-timeout 1200 python bench.py --steps 3 --warmup 3 --legs none --no-cpu-baseline > gpurun_out/e2e1.json 2> gpurun_out/e2e1.err; echo rc=$?
-timeout 1200 python bench.py --gpus 2 --steps 3 --warmup 3 --legs none --no-cpu-baseline > gpurun_out/e2e2.json 2> gpurun_out/e2e2.err; echo rc=$?
-python - <<'PY'
-import json
-for f in ("gpurun_out/e2e1.json", "gpurun_out/e2e2.json"):
-    d = json.load(open(f))
-    print(f, d["n_gpus"], round(d["value"] / 1e9, 3), round(d["e2e"]["value"] / 1e9, 3), d["e2e"]["ms_per_step"], d["ms_per_step"], d["parity"]["match"])
-PY
+# ncu --set full of the C4 d = 65536 op-engine launches (prefill run_trace + drain, timed run_ops)
+export PYTHONPATH=.
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_trace_bank -c 4 -o /tmp/c4v2 -f python tools/probe_c4.py --ds 65536 --batches 64 --c1 0 > gpurun_out/c4v2.log 2>&1; echo ncu=$?
+python tools/ncu_summarize.py /tmp/c4v2.ncu-rep gpurun_out/r02_ncu_c4_d65536_v2
+ncu -i /tmp/c4v2.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum > gpurun_out/r02_ncu_c4_d65536_v2_raw.csv 2>&1
+ls -la gpurun_out | grep c4
