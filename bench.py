@@ -248,6 +248,15 @@ def traffic_from_profiles():
         return None
 
 
+def c4_traffic_from_profiles():
+    p = os.path.join(ROOT, "profiles", "ncu_c4_summary.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
 def golden():
     try:
         with open(GOLDEN) as f:
@@ -468,6 +477,13 @@ def leg_c4(P, gen, dev, peak, ds, cpu):
                "us_per_batch": ms * 1e3 / nb, "prefill_s": pre_s,
                "roofline": {"achieved_gbs": 24 * ups / 1e9, "frac": 24 * ups / 1e9 / peak,
                             "alg_bytes_per_update": 24}}
+        tr = c4_traffic_from_profiles()
+        if tr and tr.get("d") == d:
+            # DRAM bytes per update from the committed ncu capture of this
+            # configuration (cold caches), next to the structural cascade model
+            rec["roofline"]["traffic_bytes_per_update"] = tr["dram_bytes_per_update"]
+            rec["roofline"]["traffic_source"] = tr["source"]
+            rec["roofline"]["structural_bytes_per_update"] = tr["structural_bytes_per_update"]
         # parity: extract a prefix and compare with numpy's (p_now, key) order
         m = 1_000_000 if d == ds[-1] else 10_000
         thr = np.partition(pr, m)[m]
