@@ -171,3 +171,17 @@ def test_resident_kernel_idle_exit_and_modes(pbh):
     assert eng.persist_profile()["launches"] == 3
     assert eng.live_size() == 3
     eng.close()
+
+
+def test_close_while_resident_then_reuse_device(pbh, O):
+    # destroy with the resident kernel still running (it is stopped and its
+    # state saved first), then a new heap on the same device works
+    for _ in range(3):
+        eng = pbh.Engine(pbh.EngineConfig(d=4, debug_assertions=True))
+        eng.set_persistent(1000000)
+        for v in range(50):
+            eng.update((v, 1000 - v))
+        assert tuple(eng.extract_min()) == (49, 951)
+        eng.close()  # no other call in between: the kernel is resident here
+    tr = O.gen_legal_trace(500, 4, 77)
+    check(pbh, O, tr, 4, 200, debug=True)
