@@ -359,9 +359,9 @@ def leg_c3(P, g, ctx_dev, peak, want, cpu):
 
 
 def leg_c2(P, gen, dev, peak, want, cpu):
-    """configs[1]: 4096^2 grid, source 0: exact par_dijkstra and the opt-in
-    threshold multi-extraction mode; the textbook reference_dijkstra of the
-    reference timed on one host thread."""
+    """configs[1]: 4096^2 grid, source 0: exact par_dijkstra, the opt-in
+    threshold multi-extraction mode and the device Bellman-Ford; the textbook
+    reference_dijkstra of the reference timed on one host thread."""
     g = gen.grid(4096, 4096, 1)
     V, E = g.vertex_count, g.edge_count
     ctx = P.SsspContext(g, device=dev, max_sources=1)
@@ -383,8 +383,14 @@ def leg_c2(P, gen, dev, peak, want, cpu):
     ctx.close()
     rec["threshold_mode"] = {"ms": tms, "edges_per_s": E / (tms / 1e3), "batches": rt.rounds,
                              "speedup_over_exact": ms / tms}
+    # the device Bellman-Ford frontier sweep (bellman_ford, sssp.hpp:37; the
+    # reference's cross-check solver), timed on the device like the others
+    rb, scanned, bms = P.bellman_ford(g, 0, device=dev, with_parent=False)
+    rec["device_bellman_ford"] = {"ms": bms, "edges_scanned": scanned, "rounds": rb.rounds,
+                                  "edges_per_s": E / (bms / 1e3)}
     if want:
         par["threshold_dist"] = P.distance_checksum(rt.dist) == want["dist_checksum"][0]
+        par["bellman_ford_dist"] = P.distance_checksum(rb.dist) == want["dist_checksum"][0]
         rec["parity"] = par
         rec["match"] = all(par.values())
     if cpu:
