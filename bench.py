@@ -531,7 +531,36 @@ def leg_api_latency(P, dev, n_calls=2000):
     the calls through mapped host memory) and one launch per call."""
     out = _api_latency(P, dev, n_calls, 200)
     out["one_launch_per_call"] = _api_latency(P, dev, n_calls, 0)
+    cpp = _api_latency_cpp(dev, n_calls)
+    if cpp:
+        out["cpp"] = cpp
     return out
+
+
+def _api_latency_cpp(dev, n_calls):
+    """The same calls through the C++ drop-in (tools/api_latency.cpp, built
+    here with g++ against libpbh_gpu.so), without the interpreter."""
+    import shutil
+    import subprocess
+    import tempfile
+    if not shutil.which("g++"):
+        return None
+    lib = os.path.join(ROOT, "paper_1908_09378_b200")
+    exe = os.path.join(tempfile.mkdtemp(), "api_latency")
+    try:
+        subprocess.run(["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tools", "api_latency.cpp"), "-L" + lib, "-lpbh_gpu",
+                        "-Wl,-rpath," + lib, "-o", exe], check=True, capture_output=True, timeout=300)
+        env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", str(dev)))
+        res = {}
+        for idle, key in ((200, "persistent"), (0, "one_launch_per_call")):
+            r = subprocess.run([exe, str(n_calls), str(idle)], capture_output=True, text=True,
+                               timeout=300, env=env)
+            if r.returncode == 0:
+                res[key] = json.loads(r.stdout.strip().splitlines()[-1])
+        return res or None
+    except (subprocess.SubprocessError, OSError, ValueError):
+        return None
 
 
 def _api_latency(P, dev, n_calls, idle_us):
